@@ -1,0 +1,183 @@
+/*
+ * hp_capi.h — the C-ABI boundary of the B200 adaptive-bitwidth linear path.
+ *
+ * Everything the reference's planning interfaces (proj/include/hetplan/…)
+ * need from the GPU goes through these entry points: plain pointers and
+ * sizes, no C++ or torch types, no exceptions across the ABI, reentrant,
+ * stream-ordered. Status codes mirror the reference CLI's exit codes
+ * (/root/reference/proj/tools/hetplan_main.cpp:39-42): 0 ok, 2 invalid
+ * input, 3 infeasible, 4 time-limit; CUDA/NCCL failures get their own codes.
+ * The C++ wrappers in include/hetplan/{quant,qlinear,plan,runtime} rethrow
+ * them as the reference's exception types (std::invalid_argument,
+ * hetplan::infeasible_error, std::runtime_error).
+ *
+ * All device pointers are caller-owned. There is no CPU fallback: on a box
+ * without a usable sm_100 device every compute entry point returns HP_ECUDA.
+ *
+ * Which reference interface each entry point replaces is noted per function
+ * (the reference has no GPU code at all — /root/reference/SPEC.md:8 — so
+ * "replaces" means: the CPU function whose semantics the kernel reproduces).
+ */
+#ifndef HP_CAPI_H
+#define HP_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    HP_OK = 0,
+    HP_EINTERNAL = 1,
+    HP_EINVAL = 2,       /* reference exit code 2 (std::invalid_argument) */
+    HP_EINFEASIBLE = 3,  /* reference exit code 3 (infeasible_error)      */
+    HP_ETIMEOUT = 4,     /* reference exit code 4 (time-limited incumbent)*/
+    HP_ECUDA = 5,
+    HP_ENCCL = 6
+} hp_status;
+
+/* Opaque CUDA stream (cudaStream_t); NULL = legacy default stream. */
+typedef void* hp_stream;
+
+/* Thread-local message of the last failing call on this thread. */
+const char* hp_last_error(void);
+/* ABI version; bumped on any layout or signature change. */
+int hp_abi_version(void);
+/* 1 if a CUDA device with compute capability 10.x is usable, else 0. */
+int hp_device_ok(void);
+
+/* Quantizer scheme / rounding — numeric values match the order of
+ * hetplan::indicator::quant_scheme / rounding_mode (indicator.hpp:22-23). */
+enum { HP_ASYMMETRIC = 0, HP_SYMMETRIC = 1 };
+enum { HP_NEAREST = 0, HP_STOCHASTIC = 1 };
+/* Execution phase (hetplan::memcost::phase, memcost.hpp:14). */
+enum { HP_PREFILL = 0, HP_DECODE = 1 };
+/* Fused epilogue flags for hp_qlinear. */
+enum { HP_EPI_NONE = 0, HP_EPI_RELU = 1 };
+
+/* ---- packed weight format ------------------------------------------------
+ * W is [n_out × k_in] bf16 row-major (y = x · Wᵀ). Groups of HP_GROUP
+ * consecutive elements along k_in share one step (scale) and zero.
+ * Tiles of 128 rows × 128 k are stored contiguously; see DESIGN.md §3 for
+ * the bit layout. For n_out % 128 == 0 and k_in % 128 == 0 the packed
+ * buffer is exactly ceil(n_out·k_in·bits/8) bytes — the packed-size contract
+ * of memcost::decoder_weight_bytes (memcost.cpp:15-18,30-36). Scales and
+ * zeros are fp32, one per (row, group), stored tile-major as well.       */
+#define HP_GROUP 128
+
+typedef struct {
+    int64_t n_out;
+    int64_t k_in;
+    int32_t bits;    /* 3, 4, 8 or 16 (16 = bf16 passthrough)           */
+    int32_t scheme;  /* HP_ASYMMETRIC / HP_SYMMETRIC                     */
+    const void* packed; /* hp_packed_bytes() bytes                       */
+    const float* scale; /* hp_scale_count() floats (NULL when bits==16)  */
+    const float* zero;  /* hp_scale_count() floats, asymmetric only      */
+} hp_qweight;
+
+int64_t hp_packed_bytes(int64_t n_out, int64_t k_in, int bits);
+int64_t hp_scale_count(int64_t n_out, int64_t k_in);
+
+/* K1 — group-wise quantize + pack (bit-exact with the reference quantizer
+ * applied per group: /root/reference/proj/src/indicator.cpp:19-56 with
+ * scaling_factor :82-91; round-to-nearest only, ties half-up).
+ *   w       device bf16 [n_out × ldw], ldw ≥ k_in
+ *   packed  device, hp_packed_bytes()      scale/zero device, hp_scale_count()
+ *   step64/zero64  optional device fp64 [n_out × ceil(k_in/128)] row-major,
+ *           the reference's step and grid origin per group (for parity).
+ * bits == 16 stores bf16 verbatim in tile order (reference: quantize() is the
+ * identity at 16, indicator.cpp:21).                                       */
+hp_status hp_quant_pack(const void* w, int64_t n_out, int64_t k_in,
+                        int64_t ldw, int bits, int scheme, int rounding,
+                        void* packed, float* scale, float* zero,
+                        double* step64, double* zero64, hp_stream stream);
+
+/* Unpack (parity/inspection): stored codes as u8 [n_out × k_in] row-major
+ * (symmetric codes carry the +hi offset, hi = 2^(bits-1)-1), and fp32
+ * scale/zero [n_out × groups] row-major. For bits==16, `codes` receives the
+ * bf16 words (2 bytes per element). Any output may be NULL.             */
+hp_status hp_quant_unpack(const hp_qweight* w, void* codes, float* scale_rm,
+                          float* zero_rm, hp_stream stream);
+
+/* Dequantize to bf16 [n_out × k_in]: zero + code·step rounded to bf16
+ * (reference dequant formula indicator.cpp:53; the GEMM kernels use the
+ * same per-element arithmetic).                                          */
+hp_status hp_dequant(const hp_qweight* w, void* w_bf16, hp_stream stream);
+
+/* K2 — quantization-variance indicator statistics for one operator
+ * (hetplan::indicator::operator_stats, indicator.hpp:31-38):
+ *   stats5[0] = d_w = n_out·k_in, [1] = w_min, [2] = w_max (exact),
+ *   [3] = x_mean, [4] = x_var (population, fp64 accumulation) over all
+ *   tokens·k_in elements of the calibration input x [tokens × ldx] bf16.
+ * stats5 is a DEVICE pointer (5 doubles). x may be NULL (x stats = 0).   */
+hp_status hp_indicator_stats(const void* w, int64_t n_out, int64_t k_in,
+                             int64_t ldw, const void* x, int64_t tokens,
+                             int64_t ldx, double* stats5, hp_stream stream);
+
+/* K3 / K4 — y[m × n_out] = epi(x[m × k_in] · dequant(W)ᵀ) (+ residual).
+ *   x   device bf16, row stride ldx elements (ldx % 8 == 0)
+ *   y   device bf16, row stride ldy;  residual (nullable) stride ldr
+ *   phase HP_DECODE selects the skinny-M (M = ξ) schedule with split-K,
+ *   HP_PREFILL the wide-M tile schedule. Both run tcgen05 MMAs with the
+ *   dequantized weights in tensor memory.
+ *   workspace: hp_qlinear_workspace_bytes() bytes of device memory (may be
+ *   NULL when that is 0), zero-initialised once by the caller; kernels
+ *   leave it zeroed again on exit.                                         */
+size_t hp_qlinear_workspace_bytes(const hp_qweight* w, int64_t m, int phase);
+hp_status hp_qlinear(const hp_qweight* w, const void* x, int64_t ldx,
+                     int64_t m, void* y, int64_t ldy, const void* residual,
+                     int64_t ldr, int epilogue, int phase, void* workspace,
+                     size_t workspace_bytes, hp_stream stream);
+
+/* ---- pipeline executor (one process per GPU, NCCL P2P at boundaries) ----
+ * plan_json: the reference plan document (hetplan_main.cpp:190-224);
+ * stage r of the plan runs on this rank. nccl_id: 128-byte ncclUniqueId
+ * produced by hp_nccl_unique_id on rank 0 and broadcast by the caller.
+ * The schedule follows pipesim::make_schedule semantics
+ * (/root/reference/proj/src/pipesim.cpp:22-46).                           */
+typedef struct hp_pipeline hp_pipeline;
+hp_status hp_nccl_unique_id(void* out128);
+hp_status hp_pipeline_create(const char* plan_json, const char* model_json,
+                             int rank, int world, const void* nccl_id,
+                             uint64_t seed, hp_pipeline** out);
+/* Run one serving round: B requests, prompt s, n generated tokens. Host
+ * buffers: prompt activations in (stage 0 only; [B × s × h1] bf16, may be
+ * NULL for synthetic), final hidden states out (last stage only; [B × h1]
+ * bf16 of the last decode step, may be NULL). Fills timing[0..3] with
+ * {makespan_s, prefill_s, decode_s, h2d_d2h_s} measured with CUDA events. */
+hp_status hp_pipeline_run(hp_pipeline* p, const void* host_in, void* host_out,
+                          double* timing4);
+/* Per-stage measured costs {pre_s, dec_s, comm_pre_s, comm_dec_s} of the
+ * last run, for comparison with pipesim::simulate.                        */
+hp_status hp_pipeline_stage_costs(hp_pipeline* p, double* out4);
+void hp_pipeline_destroy(hp_pipeline* p);
+
+/* ---- host planning helpers (drop-in hetplan:: library, plain types) -----
+ * model9 = {num_layers, h1, h2, num_heads, vocab_s, pos_s, d_t, d_p,
+ * norm(0 standard, 1 rms)}. Text outputs are NUL-terminated into out/cap.  */
+hp_status hp_host_scaling_factor(double w_min, double w_max, int bit, int scheme,
+                                 double* out);
+hp_status hp_host_g_of_x(double mean, double var, int rounding, double* out);
+hp_status hp_host_indicator_csv(const char* stats_csv, const int* bits, int nbits,
+                                int scheme, int rounding, char* out, int64_t cap);
+/* omega [n_layers × nbits] from per-op stats5 (K2 output layout),
+ * ops in qkv,out,fc1,fc2 order (indicator.cpp:99-127 op order).         */
+hp_status hp_host_omega_from_stats(const double* stats5_per_op, int n_layers,
+                                   int ops_per_layer, const int* bits, int nbits,
+                                   int scheme, int rounding, double* omega_out);
+hp_status hp_host_memcost(const int64_t* model9, int bit, int64_t v, int64_t s,
+                          int64_t n, int64_t* out3);
+hp_status hp_host_preset(const char* name, int64_t* model9);
+hp_status hp_host_make_schedule(int B, int eta, int xi, int* sizes, int* groups,
+                                int* n_batches, int* n_groups, int cap);
+hp_status hp_host_simulate(const double* costs4, int n_stages, int B, int eta,
+                           int xi, int n, double* out4, double* busy,
+                           double* timeline, int64_t timeline_cap);
+hp_status hp_host_plan_check(const char* plan_json, char* out, int64_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HP_CAPI_H */

@@ -1,0 +1,123 @@
+"""ctypes binding of the C-ABI (include/hp_capi.h).
+
+This is the only way Python reaches the product: every GPU entry point is a
+call into libhetplan_b200.so. If the library is missing, importing this
+module raises — there is no Python or CPU fallback for the path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libhetplan_b200.so"
+
+HP_OK, HP_EINTERNAL, HP_EINVAL, HP_EINFEASIBLE, HP_ETIMEOUT, HP_ECUDA, HP_ENCCL = 0, 1, 2, 3, 4, 5, 6
+HP_ASYMMETRIC, HP_SYMMETRIC = 0, 1
+HP_NEAREST, HP_STOCHASTIC = 0, 1
+HP_PREFILL, HP_DECODE = 0, 1
+HP_EPI_NONE, HP_EPI_RELU = 0, 1
+
+
+class HPError(RuntimeError):
+    """Raised for any non-zero hp_status; `.status` holds the code."""
+
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"hp_status {status}: {msg}")
+        self.status = status
+
+
+class InvalidArgument(HPError, ValueError):
+    """HP_EINVAL — the reference's std::invalid_argument."""
+
+
+class Infeasible(HPError):
+    """HP_EINFEASIBLE — the reference's hetplan::infeasible_error."""
+
+
+class hp_qweight(C.Structure):
+    _fields_ = [
+        ("n_out", C.c_int64),
+        ("k_in", C.c_int64),
+        ("bits", C.c_int32),
+        ("scheme", C.c_int32),
+        ("packed", C.c_void_p),
+        ("scale", C.c_void_p),
+        ("zero", C.c_void_p),
+    ]
+
+
+def _load() -> C.CDLL:
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the product has no fallback path)")
+    lib = C.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | os.RTLD_GLOBAL)
+    v, i64, i32, d, p = C.c_void_p, C.c_int64, C.c_int, C.c_double, C.c_char_p
+    P = C.POINTER
+    sig = {
+        "hp_last_error": (p, []),
+        "hp_abi_version": (i32, []),
+        "hp_device_ok": (i32, []),
+        "hp_packed_bytes": (i64, [i64, i64, i32]),
+        "hp_scale_count": (i64, [i64, i64]),
+        "hp_quant_pack": (i32, [v, i64, i64, i64, i32, i32, i32, v, v, v, v, v, v]),
+        "hp_quant_unpack": (i32, [P(hp_qweight), v, v, v, v]),
+        "hp_dequant": (i32, [P(hp_qweight), v, v]),
+        "hp_indicator_stats": (i32, [v, i64, i64, i64, v, i64, i64, v, v]),
+        "hp_qlinear_workspace_bytes": (C.c_size_t, [P(hp_qweight), i64, i32]),
+        "hp_qlinear": (i32, [P(hp_qweight), v, i64, i64, v, i64, v, i64, i32, i32, v, C.c_size_t, v]),
+        "hp_host_scaling_factor": (i32, [d, d, i32, i32, P(d)]),
+        "hp_host_g_of_x": (i32, [d, d, i32, P(d)]),
+        "hp_host_indicator_csv": (i32, [p, P(i32), i32, i32, i32, C.c_char_p, i64]),
+        "hp_host_omega_from_stats": (i32, [P(d), i32, i32, P(i32), i32, i32, i32, P(d)]),
+        "hp_host_memcost": (i32, [P(i64), i32, i64, i64, i64, P(i64)]),
+        "hp_host_preset": (i32, [p, P(i64)]),
+        "hp_host_make_schedule": (i32, [i32, i32, i32, P(i32), P(i32), P(i32), P(i32), i32]),
+        "hp_host_simulate": (i32, [P(d), i32, i32, i32, i32, i32, P(d), P(d), v, i64]),
+        "hp_host_plan_check": (i32, [p, C.c_char_p, i64]),
+    }
+    optional = {
+        "hp_nccl_unique_id": (i32, [v]),
+        "hp_pipeline_create": (i32, [p, p, i32, i32, v, C.c_uint64, P(v)]),
+        "hp_pipeline_run": (i32, [v, v, v, P(d)]),
+        "hp_pipeline_stage_costs": (i32, [v, P(d)]),
+        "hp_pipeline_destroy": (None, [v]),
+    }
+    for name, (res, args) in list(sig.items()) + list(optional.items()):
+        if not hasattr(lib, name):
+            if name in sig:
+                raise ImportError(f"{LIB_PATH} does not export {name}")
+            continue
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()
+
+EXPORTED = [
+    "hp_last_error", "hp_abi_version", "hp_device_ok", "hp_packed_bytes", "hp_scale_count",
+    "hp_quant_pack", "hp_quant_unpack", "hp_dequant", "hp_indicator_stats",
+    "hp_qlinear_workspace_bytes", "hp_qlinear", "hp_host_scaling_factor", "hp_host_g_of_x",
+    "hp_host_indicator_csv", "hp_host_omega_from_stats", "hp_host_memcost", "hp_host_preset",
+    "hp_host_make_schedule", "hp_host_simulate", "hp_host_plan_check", "hp_nccl_unique_id",
+    "hp_pipeline_create", "hp_pipeline_run", "hp_pipeline_stage_costs", "hp_pipeline_destroy",
+]
+
+
+def check(status: int) -> None:
+    if status == HP_OK:
+        return
+    msg = (lib.hp_last_error() or b"").decode(errors="replace")
+    if status == HP_EINVAL:
+        raise InvalidArgument(status, msg)
+    if status == HP_EINFEASIBLE:
+        raise Infeasible(status, msg)
+    raise HPError(status, msg)
+
+
+def device_ok() -> bool:
+    return bool(lib.hp_device_ok())

@@ -1,0 +1,258 @@
+// C-ABI entry points (include/hp_capi.h): argument validation, error
+// mapping (exceptions never cross the ABI), TMA descriptor encoding and
+// kernel dispatch. No CPU fallback: without a usable sm_100 device every
+// compute entry point fails with HP_ECUDA.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "hp_capi.h"
+#include "layout.cuh"
+
+namespace hp {
+cudaError_t launch_quant_pack(const void* w, int64_t n_out, int64_t k_in, int64_t ldw,
+                              int bits, int sym, void* packed, float* scale, float* zero,
+                              double* step64, double* zero64, cudaStream_t st);
+cudaError_t launch_unpack(const void* packed, const float* scale, const float* zero,
+                          int64_t n_out, int64_t k_in, int bits, void* codes,
+                          float* scale_rm, float* zero_rm, cudaStream_t st);
+cudaError_t launch_dequant(const void* packed, const float* scale, const float* zero,
+                           int64_t n_out, int64_t k_in, int bits, int sym, void* out,
+                           cudaStream_t st);
+size_t stats_scratch_bytes(int nbw, int nbx);
+cudaError_t launch_stats(const void* w, int64_t n_out, int64_t k_in, int64_t ldw,
+                         const void* x, int64_t tokens, int64_t ldx, double* out,
+                         void* scratch, int nbw, int nbx, cudaStream_t st);
+struct qgemm_plan {
+    int bn, mt, splits, gps, units, grid;
+    size_t workspace;
+};
+qgemm_plan plan_qgemm(int64_t n_out, int64_t k_in, int64_t m, int phase);
+cudaError_t launch_qgemm(const CUtensorMap& map, const qgemm_plan& p, int bits, bool sym,
+                         const void* packed, const float* scale, const float* zero,
+                         int64_t n_out, int64_t k_in, int64_t m, void* y, int64_t ldy,
+                         const void* res, int64_t ldr, int epi, void* workspace,
+                         cudaStream_t st);
+}  // namespace hp
+
+namespace {
+thread_local std::string g_error;
+}  // namespace
+
+namespace hp_detail {
+void set_error(const std::string& msg) { g_error = msg; }
+}  // namespace hp_detail
+
+namespace {
+
+hp_status fail(hp_status s, const std::string& msg) {
+    g_error = msg;
+    return s;
+}
+
+hp_status cuda_status(cudaError_t e, const char* where) {
+    if (e == cudaSuccess) return HP_OK;
+    return fail(HP_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+bool bits_ok(int b) { return b == 3 || b == 4 || b == 8 || b == 16; }
+
+int device_ok_cached() {
+    static int ok = -1;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    if (ok < 0) {
+        int dev = 0, major = 0;
+        ok = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) ==
+                cudaSuccess &&
+            major == 10)
+            ok = 1;
+        cudaGetLastError();
+    }
+    return ok;
+}
+
+hp_status need_device() {
+    if (!device_ok_cached())
+        return fail(HP_ECUDA, "no usable sm_100 (B200) device; the CPU path is not a fallback");
+    return HP_OK;
+}
+
+using encode_fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                               const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                               CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+encode_fn get_encode() {
+    static encode_fn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<encode_fn>(p);
+        cudaGetLastError();
+    });
+    return fn;
+}
+
+// Activations [rows × k] bf16, row stride ld elements; box 64 k × box_rows,
+// 128-byte swizzle (the UMMA K-major SW128 layout), OOB -> zero.
+hp_status make_act_map(CUtensorMap* map, const void* x, int64_t k, int64_t rows,
+                       int64_t ld, int box_rows) {
+    encode_fn enc = get_encode();
+    if (!enc) return fail(HP_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
+    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x), dims,
+                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        return fail(HP_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+    return HP_OK;
+}
+
+hp_status check_qweight(const hp_qweight* w) {
+    if (!w) return fail(HP_EINVAL, "qweight is NULL");
+    if (w->n_out <= 0 || w->k_in <= 0) return fail(HP_EINVAL, "qweight: empty shape");
+    if (!bits_ok(w->bits)) return fail(HP_EINVAL, "qweight: bits must be 3, 4, 8 or 16");
+    if (w->scheme != HP_ASYMMETRIC && w->scheme != HP_SYMMETRIC)
+        return fail(HP_EINVAL, "qweight: unknown scheme");
+    if (!w->packed) return fail(HP_EINVAL, "qweight: packed is NULL");
+    if (w->bits != 16 && !w->scale) return fail(HP_EINVAL, "qweight: scale is NULL");
+    if (w->bits != 16 && w->scheme == HP_ASYMMETRIC && !w->zero)
+        return fail(HP_EINVAL, "qweight: asymmetric weights need zero");
+    if (w->n_out > (1LL << 30) || w->k_in > (1LL << 30))
+        return fail(HP_EINVAL, "qweight: dimension too large");
+    return HP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hp_last_error(void) { return g_error.c_str(); }
+
+int hp_abi_version(void) { return 1; }
+
+int hp_device_ok(void) { return device_ok_cached(); }
+
+int64_t hp_packed_bytes(int64_t n_out, int64_t k_in, int bits) {
+    if (n_out <= 0 || k_in <= 0 || !bits_ok(bits)) return -1;
+    return hp::ceil_div64(n_out, 128) * hp::ceil_div64(k_in, 128) * hp::tile_bytes(bits);
+}
+
+int64_t hp_scale_count(int64_t n_out, int64_t k_in) {
+    if (n_out <= 0 || k_in <= 0) return -1;
+    return hp::ceil_div64(n_out, 128) * hp::ceil_div64(k_in, 128) * 128;
+}
+
+hp_status hp_quant_pack(const void* w, int64_t n_out, int64_t k_in, int64_t ldw, int bits,
+                        int scheme, int rounding, void* packed, float* scale, float* zero,
+                        double* step64, double* zero64, hp_stream stream) {
+    if (!w || !packed) return fail(HP_EINVAL, "quant_pack: NULL w or packed");
+    if (n_out <= 0 || k_in <= 0) return fail(HP_EINVAL, "quant_pack: empty shape");
+    if (ldw < k_in) return fail(HP_EINVAL, "quant_pack: ldw < k_in");
+    if (!bits_ok(bits)) return fail(HP_EINVAL, "quant_pack: bits must be 3, 4, 8 or 16");
+    if (scheme != HP_ASYMMETRIC && scheme != HP_SYMMETRIC)
+        return fail(HP_EINVAL, "quant_pack: unknown scheme");
+    if (rounding != HP_NEAREST)
+        return fail(HP_EINVAL,
+                    "quant_pack: only round-to-nearest is supported on the GPU (the "
+                    "reference's stochastic rounding draws a sequential mt19937_64 stream)");
+    if (bits != 16 && !scale) return fail(HP_EINVAL, "quant_pack: scale is NULL");
+    if ((step64 == nullptr) != (zero64 == nullptr))
+        return fail(HP_EINVAL, "quant_pack: step64 and zero64 go together");
+    if (hp_status s = need_device()) return s;
+    return cuda_status(hp::launch_quant_pack(w, n_out, k_in, ldw, bits, scheme, packed, scale,
+                                             zero, step64, zero64,
+                                             static_cast<cudaStream_t>(stream)),
+                       "quant_pack");
+}
+
+hp_status hp_quant_unpack(const hp_qweight* w, void* codes, float* scale_rm, float* zero_rm,
+                          hp_stream stream) {
+    if (hp_status s = check_qweight(w)) return s;
+    if (hp_status s = need_device()) return s;
+    return cuda_status(hp::launch_unpack(w->packed, w->scale, w->zero, w->n_out, w->k_in,
+                                         w->bits, codes, scale_rm, zero_rm,
+                                         static_cast<cudaStream_t>(stream)),
+                       "quant_unpack");
+}
+
+hp_status hp_dequant(const hp_qweight* w, void* w_bf16, hp_stream stream) {
+    if (hp_status s = check_qweight(w)) return s;
+    if (!w_bf16) return fail(HP_EINVAL, "dequant: NULL output");
+    if (hp_status s = need_device()) return s;
+    return cuda_status(hp::launch_dequant(w->packed, w->scale, w->zero, w->n_out, w->k_in,
+                                          w->bits, w->scheme == HP_SYMMETRIC, w_bf16,
+                                          static_cast<cudaStream_t>(stream)),
+                       "dequant");
+}
+
+hp_status hp_indicator_stats(const void* w, int64_t n_out, int64_t k_in, int64_t ldw,
+                             const void* x, int64_t tokens, int64_t ldx, double* stats5,
+                             hp_stream stream) {
+    if (!w || !stats5) return fail(HP_EINVAL, "indicator_stats: NULL w or stats5");
+    if (n_out <= 0 || k_in <= 0) return fail(HP_EINVAL, "indicator_stats: empty weight");
+    if (ldw < k_in) return fail(HP_EINVAL, "indicator_stats: ldw < k_in");
+    if (x && (tokens <= 0 || ldx < k_in))
+        return fail(HP_EINVAL, "indicator_stats: bad calibration shape");
+    if (hp_status s = need_device()) return s;
+    auto st = static_cast<cudaStream_t>(stream);
+    const int nbw = 296, nbx = x ? 296 : 0;
+    const size_t bytes = hp::stats_scratch_bytes(nbw, nbx);
+    void* scratch = nullptr;
+    cudaError_t e = cudaMallocAsync(&scratch, bytes, st);
+    if (e != cudaSuccess) return cuda_status(e, "indicator_stats alloc");
+    e = cudaMemsetAsync(scratch, 0, 256, st);
+    if (e == cudaSuccess)
+        e = hp::launch_stats(w, n_out, k_in, ldw, x, tokens, ldx, stats5, scratch, nbw, nbx, st);
+    cudaFreeAsync(scratch, st);
+    return cuda_status(e, "indicator_stats");
+}
+
+size_t hp_qlinear_workspace_bytes(const hp_qweight* w, int64_t m, int phase) {
+    if (!w || w->n_out <= 0 || w->k_in <= 0 || m <= 0) return 0;
+    return hp::plan_qgemm(w->n_out, w->k_in, m, phase).workspace;
+}
+
+hp_status hp_qlinear(const hp_qweight* w, const void* x, int64_t ldx, int64_t m, void* y,
+                     int64_t ldy, const void* residual, int64_t ldr, int epilogue, int phase,
+                     void* workspace, size_t workspace_bytes, hp_stream stream) {
+    if (hp_status s = check_qweight(w)) return s;
+    if (m <= 0) return fail(HP_EINVAL, "qlinear: m must be positive");
+    if (!x || !y) return fail(HP_EINVAL, "qlinear: NULL x or y");
+    if (ldx < w->k_in || ldx % 8 != 0 || (reinterpret_cast<uintptr_t>(x) & 15))
+        return fail(HP_EINVAL, "qlinear: x must be 16-byte aligned with ldx >= k_in, ldx % 8 == 0");
+    if (ldy < w->n_out) return fail(HP_EINVAL, "qlinear: ldy < n_out");
+    if (residual && ldr < w->n_out) return fail(HP_EINVAL, "qlinear: ldr < n_out");
+    if (phase != HP_PREFILL && phase != HP_DECODE) return fail(HP_EINVAL, "qlinear: bad phase");
+    if (epilogue & ~HP_EPI_RELU) return fail(HP_EINVAL, "qlinear: unknown epilogue flags");
+    if (m > (1LL << 30)) return fail(HP_EINVAL, "qlinear: m too large");
+    if (hp_status s = need_device()) return s;
+    const hp::qgemm_plan p = hp::plan_qgemm(w->n_out, w->k_in, m, phase);
+    if (p.workspace > 0 && (workspace == nullptr || workspace_bytes < p.workspace))
+        return fail(HP_EINVAL, "qlinear: workspace too small (need " +
+                                   std::to_string(p.workspace) + " bytes)");
+    CUtensorMap map;
+    if (hp_status s = make_act_map(&map, x, w->k_in, m, ldx, p.bn)) return s;
+    return cuda_status(hp::launch_qgemm(map, p, w->bits, w->scheme == HP_SYMMETRIC, w->packed,
+                                        w->scale, w->zero, w->n_out, w->k_in, m, y, ldy,
+                                        residual, ldr, epilogue, workspace,
+                                        static_cast<cudaStream_t>(stream)),
+                       "qlinear");
+}
+
+}  // extern "C"

@@ -1,0 +1,208 @@
+// extern "C" surface of the host planning library (include/hp_capi.h,
+// "host planning helpers"): the drop-in hetplan:: functions exposed with
+// plain types so the parity tests can drive them next to the reference
+// build. Exceptions are mapped to hp_status like the rest of the ABI.
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "hetplan/config.hpp"
+#include "hetplan/indicator/indicator.hpp"
+#include "hetplan/memcost/memcost.hpp"
+#include "hetplan/pipesim/pipesim.hpp"
+#include "hetplan/plan/plan_io.hpp"
+#include "hetplan/types.hpp"
+#include "hp_capi.h"
+
+namespace hp_detail {
+void set_error(const std::string& msg);  // capi.cu
+}
+
+namespace {
+
+hp_status from_exception(const std::exception& e) {
+    hp_detail::set_error(e.what());
+    if (dynamic_cast<const hetplan::infeasible_error*>(&e)) return HP_EINFEASIBLE;
+    if (dynamic_cast<const std::invalid_argument*>(&e)) return HP_EINVAL;
+    return HP_EINTERNAL;
+}
+
+hp_status put_string(const std::string& s, char* out, int64_t cap) {
+    if (static_cast<int64_t>(s.size()) + 1 > cap) {
+        hp_detail::set_error("output buffer too small: need " + std::to_string(s.size() + 1));
+        return HP_EINVAL;
+    }
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return HP_OK;
+}
+
+hetplan::model_spec model_of(const int64_t* f) {
+    hetplan::model_spec m;
+    m.name = "custom";
+    m.num_layers = static_cast<int>(f[0]);
+    m.h1 = f[1];
+    m.h2 = f[2];
+    m.num_heads = static_cast<int>(f[3]);
+    m.vocab_s = f[4];
+    m.pos_s = f[5];
+    m.d_t = f[6];
+    m.d_p = f[7];
+    m.norm = f[8] == 0 ? hetplan::norm_kind::standard : hetplan::norm_kind::rms;
+    return m;
+}
+
+hetplan::indicator::quantizer_spec qspec(int scheme, int rounding) {
+    hetplan::indicator::quantizer_spec q;
+    q.scheme = scheme == HP_ASYMMETRIC ? hetplan::indicator::quant_scheme::asymmetric
+                                       : hetplan::indicator::quant_scheme::symmetric;
+    q.rounding = rounding == HP_NEAREST ? hetplan::indicator::rounding_mode::nearest
+                                        : hetplan::indicator::rounding_mode::stochastic;
+    return q;
+}
+
+}  // namespace
+
+extern "C" {
+
+hp_status hp_host_scaling_factor(double w_min, double w_max, int bit, int scheme,
+                                 double* out) {
+    try {
+        *out = hetplan::indicator::scaling_factor(w_min, w_max, bit, qspec(scheme, 0).scheme);
+        return HP_OK;
+    } catch (const std::exception& e) {
+        return from_exception(e);
+    }
+}
+
+hp_status hp_host_g_of_x(double mean, double var, int rounding, double* out) {
+    try {
+        *out = hetplan::indicator::g_of_x(mean, var, qspec(1, rounding).rounding);
+        return HP_OK;
+    } catch (const std::exception& e) {
+        return from_exception(e);
+    }
+}
+
+hp_status hp_host_indicator_csv(const char* stats_csv, const int* bits, int nbits, int scheme,
+                                int rounding, char* out, int64_t cap) {
+    try {
+        auto layers = hetplan::indicator::parse_layer_stats(stats_csv);
+        auto t = hetplan::indicator::build_indicator_table(
+            layers, hetplan::bitwidth_set(bits, bits + nbits), qspec(scheme, rounding));
+        return put_string(hetplan::indicator::serialize_indicator_table(t), out, cap);
+    } catch (const std::exception& e) {
+        return from_exception(e);
+    }
+}
+
+hp_status hp_host_omega_from_stats(const double* stats5_per_op, int n_layers, int ops_per_layer,
+                                   const int* bits, int nbits, int scheme, int rounding,
+                                   double* omega_out) {
+    try {
+        static const char* names[] = {"qkv", "out", "fc1", "fc2"};
+        std::vector<hetplan::indicator::layer_stats> layers(n_layers);
+        for (int i = 0; i < n_layers; ++i)
+            for (int o = 0; o < ops_per_layer; ++o) {
+                const double* s = stats5_per_op + 5 * (i * ops_per_layer + o);
+                layers[i].push_back({o < 4 ? names[o] : "op", static_cast<int64_t>(s[0]), s[1],
+                                     s[2], s[3], s[4]});
+            }
+        auto t = hetplan::indicator::build_indicator_table(
+            layers, hetplan::bitwidth_set(bits, bits + nbits), qspec(scheme, rounding));
+        for (int i = 0; i < n_layers; ++i)
+            for (int b = 0; b < nbits; ++b) omega_out[i * nbits + b] = t.omega[i][b];
+        return HP_OK;
+    } catch (const std::exception& e) {
+        return from_exception(e);
+    }
+}
+
+hp_status hp_host_memcost(const int64_t* model9, int bit, int64_t v, int64_t s, int64_t n,
+                          int64_t* out3) {
+    try {
+        const auto m = model_of(model9);
+        out3[0] = hetplan::memcost::embed_mem_bytes(m);
+        out3[1] = hetplan::memcost::decoder_weight_bytes(m, bit);
+        out3[2] = hetplan::memcost::kv_cache_bytes(m, v, s, n, 16);
+        return HP_OK;
+    } catch (const std::exception& e) {
+        return from_exception(e);
+    }
+}
+
+hp_status hp_host_preset(const char* name, int64_t* model9) {
+    try {
+        const auto m = hetplan::model_preset(name);
+        const int64_t f[9] = {m.num_layers, m.h1, m.h2, m.num_heads, m.vocab_s,
+                              m.pos_s, m.d_t, m.d_p, m.norm == hetplan::norm_kind::standard ? 0 : 1};
+        std::memcpy(model9, f, sizeof f);
+        return HP_OK;
+    } catch (const std::exception& e) {
+        return from_exception(e);
+    }
+}
+
+hp_status hp_host_make_schedule(int B, int eta, int xi, int* sizes, int* groups, int* n_batches,
+                                int* n_groups, int cap) {
+    try {
+        const auto s = hetplan::pipesim::make_schedule(B, eta, xi);
+        if (static_cast<int>(s.prefill_sizes.size()) > cap)
+            throw std::invalid_argument("schedule: capacity");
+        for (size_t k = 0; k < s.prefill_sizes.size(); ++k) {
+            sizes[k] = s.prefill_sizes[k];
+            groups[k] = s.group_of_prefill[k];
+        }
+        *n_batches = static_cast<int>(s.prefill_sizes.size());
+        *n_groups = s.num_groups;
+        return HP_OK;
+    } catch (const std::exception& e) {
+        return from_exception(e);
+    }
+}
+
+hp_status hp_host_simulate(const double* costs4, int n_stages, int B, int eta, int xi, int n,
+                           double* out4, double* busy, double* timeline, int64_t timeline_cap) {
+    try {
+        std::vector<hetplan::pipesim::stage_cost> st(n_stages);
+        for (int j = 0; j < n_stages; ++j)
+            st[j] = {costs4[4 * j], costs4[4 * j + 1], costs4[4 * j + 2], costs4[4 * j + 3], 0.0};
+        const auto sched = hetplan::pipesim::make_schedule(B, eta, xi);
+        const auto r = hetplan::pipesim::simulate(st, sched, n, timeline != nullptr);
+        out4[0] = r.makespan_s;
+        out4[1] = r.bubble_fraction;
+        out4[2] = hetplan::pipesim::analytic_latency(st, B, eta, xi, n);
+        out4[3] = static_cast<double>(r.timeline.size());
+        for (int j = 0; j < n_stages; ++j) busy[j] = r.stage_busy_s[j];
+        if (timeline) {
+            if (static_cast<int64_t>(r.timeline.size()) > timeline_cap)
+                throw std::invalid_argument("simulate: timeline capacity");
+            for (size_t k = 0; k < r.timeline.size(); ++k) {
+                const auto& e = r.timeline[k];
+                double* row = timeline + 6 * k;
+                row[0] = e.stage;
+                row[1] = e.kind == hetplan::pipesim::unit_kind::prefill ? 0 : 1;
+                row[2] = e.index;
+                row[3] = e.token;
+                row[4] = e.start;
+                row[5] = e.end;
+            }
+        }
+        return HP_OK;
+    } catch (const std::exception& e) {
+        return from_exception(e);
+    }
+}
+
+// Parse + validate a plan document; returns the normalised document (the
+// B200 runtime's view: stage.device = stage index) as JSON.
+hp_status hp_host_plan_check(const char* plan_json, char* out, int64_t cap) {
+    try {
+        const auto doc = hetplan::plan_io::parse_plan(plan_json);
+        hetplan::plan_io::validate(doc);
+        return put_string(hetplan::plan_io::serialize_plan(doc), out, cap);
+    } catch (const std::exception& e) {
+        return from_exception(e);
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,307 @@
+// K1 — group-wise quantize + pack (sm_100a), plus the unpack / dequant
+// utilities over the same tile layout (layout.cuh).
+//
+// Semantics follow the reference quantizer applied to each group of 128
+// consecutive weights of a row: /root/reference/proj/src/indicator.cpp:19-56
+// (minmax -> step = scaling_factor :82-91 -> snapped = floor((w-zero)/step
+// + 0.5) -> clamp [lo,hi]), all in fp64 with the reference's exact operation
+// sequence on the slow path. Round-to-nearest only (the SPEC default,
+// SPEC.md:328); stochastic rounding uses a sequential mt19937_64 stream in
+// the reference (indicator.cpp:37,50) and is rejected here.
+//
+// Fast path: x = ((float)w - (float)zero) * rcp_f32(step). Its absolute
+// error is < 1e-4 for |x| <= 255, so whenever frac(x + 0.5)
+// lies in [1e-3, 1 - 1e-3] the rounded code equals the reference's; other
+// elements (ties, near-ties, non-finite) take the exact fp64 sequence
+// __dsub_rn / __ddiv_rn / __dadd_rn / floor / clamp. About 0.3% of bf16
+// weights take the slow path.
+#include <cuda_bf16.h>
+#include <cstdint>
+
+#include "layout.cuh"
+
+namespace hp {
+
+namespace {
+
+constexpr float kTieMargin = 1e-3f;
+
+struct group_grid {
+    double step, zero, lo, hi;
+    float zero_f, rcp_f;
+};
+
+__device__ __forceinline__ group_grid make_grid(float wmin, float wmax,
+                                                int bits, bool sym) {
+    group_grid g;
+    // scaling_factor (indicator.cpp:82-91); pow(2,b)-1 is exact.
+    if (sym) {
+        const double hi = static_cast<double>((1 << (bits - 1)) - 1);
+        const double amax = fmax(fabs(static_cast<double>(wmax)),
+                                 fabs(static_cast<double>(wmin)));
+        g.step = __ddiv_rn(amax, hi);
+        g.zero = 0.0;
+        g.lo = -hi;
+        g.hi = hi;
+    } else {
+        const double hi = static_cast<double>((1 << bits) - 1);
+        g.step = __ddiv_rn(__dsub_rn(static_cast<double>(wmax),
+                                     static_cast<double>(wmin)),
+                           hi);
+        g.zero = static_cast<double>(wmin);
+        g.lo = 0.0;
+        g.hi = hi;
+    }
+    g.zero_f = static_cast<float>(g.zero);
+    g.rcp_f = 1.0f / static_cast<float>(g.step);
+    return g;
+}
+
+// Signed grid code of one element (reference quantize() inner loop).
+__device__ __forceinline__ int quant_code(float w, const group_grid& g) {
+    if (g.step == 0.0) return 0;  // flat group: out = zero (indicator.cpp:39-41)
+    const float x = (w - g.zero_f) * g.rcp_f + 0.5f;
+    const float fl = floorf(x);
+    const float fr = x - fl;
+    double sn;
+    if (fr >= kTieMargin && fr <= 1.0f - kTieMargin) {
+        sn = static_cast<double>(fl);
+    } else {
+        const double scaled =
+            __ddiv_rn(__dsub_rn(static_cast<double>(w), g.zero), g.step);
+        sn = floor(__dadd_rn(scaled, 0.5));
+    }
+    sn = sn < g.lo ? g.lo : (g.hi < sn ? g.hi : sn);  // std::clamp
+    return static_cast<int>(sn);
+}
+
+// One CTA = one 128x128 tile; thread r owns row r.
+template <int BITS>
+__global__ void __launch_bounds__(128)
+    quant_pack_kernel(const __nv_bfloat16* __restrict__ w, int64_t n_out,
+                      int64_t k_in, int64_t ldw, int G, int sym,
+                      uint8_t* __restrict__ packed, float* __restrict__ scale,
+                      float* __restrict__ zero, double* __restrict__ step64,
+                      double* __restrict__ zero64) {
+    constexpr int kPad = 8;  // bf16 elements of row padding (bank spread)
+    __shared__ __align__(16) __nv_bfloat16 tile[128][128 + kPad];
+    const int g = blockIdx.x;
+    const int64_t nt = blockIdx.y;
+    const int r = threadIdx.x;
+    const int64_t row0 = nt * 128;
+    const int64_t k0 = static_cast<int64_t>(g) * 128;
+    const int cnt = static_cast<int>(k_in - k0 < 128 ? k_in - k0 : 128);
+    const bool vec_ok = (cnt == 128) && (ldw % 8 == 0) &&
+                        ((reinterpret_cast<uintptr_t>(w) & 15) == 0);
+
+    // coalesced load: 16 lanes cover one row's 256 bytes
+    if (vec_ok) {
+#pragma unroll 4
+        for (int q = r; q < 128 * 16; q += 128) {
+            const int rr = q >> 4, cc = q & 15;
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (row0 + rr < n_out)
+                v = __ldg(reinterpret_cast<const uint4*>(w + (row0 + rr) * ldw + k0) + cc);
+            *reinterpret_cast<uint4*>(&tile[rr][cc * 8]) = v;
+        }
+    } else {
+        for (int q = r; q < 128 * 128; q += 128) {
+            const int rr = q >> 7, cc = q & 127;
+            __nv_bfloat16 v = __float2bfloat16(0.0f);
+            if (row0 + rr < n_out && cc < cnt) v = w[(row0 + rr) * ldw + k0 + cc];
+            tile[rr][cc] = v;
+        }
+    }
+    __syncthreads();
+
+    const bool row_ok = row0 + r < n_out;
+    const size_t sidx = (static_cast<size_t>(nt) * G + g) * 128 + r;
+    uint8_t* tbase = packed + (static_cast<size_t>(nt) * G + g) * tile_bytes(BITS) + r * 16;
+
+    if constexpr (BITS == 16) {
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+            *reinterpret_cast<uint4*>(tbase + c * 2048) =
+                *reinterpret_cast<const uint4*>(&tile[r][c * 8]);
+        return;
+    } else {
+        float wmin = 0.0f, wmax = 0.0f;
+        if (row_ok) {
+            wmin = __bfloat162float(tile[r][0]);
+            wmax = wmin;
+            for (int k = 1; k < cnt; ++k) {
+                const float v = __bfloat162float(tile[r][k]);
+                wmin = fminf(wmin, v);
+                wmax = fmaxf(wmax, v);
+            }
+        }
+        const group_grid gg = make_grid(wmin, wmax, BITS, sym != 0);
+        const int off = sym ? (1 << (BITS - 1)) - 1 : 0;
+        if (scale) scale[sidx] = row_ok ? static_cast<float>(gg.step) : 0.0f;
+        if (zero) zero[sidx] = row_ok ? gg.zero_f : 0.0f;
+        if (row_ok && step64) {
+            step64[(row0 + r) * G + g] = gg.step;
+            zero64[(row0 + r) * G + g] = gg.zero;
+        }
+
+        uint32_t words[BITS * 4];
+#pragma unroll
+        for (int i = 0; i < BITS * 4; ++i) words[i] = 0;
+#pragma unroll 8
+        for (int kk = 0; kk < 128; ++kk) {
+            int q = 0;  // padding / invalid rows: signed code 0
+            if (row_ok && kk < cnt) q = quant_code(__bfloat162float(tile[r][kk]), gg);
+            const uint32_t sc = static_cast<uint32_t>(q + off);
+            const code_pos p = locate_code(BITS, kk);
+            if constexpr (BITS == 3) {
+                words[p.chunk * 4 + p.word] |= (sc & 3u) << p.shift;
+                words[p.chunk2 * 4 + p.word2] |= ((sc >> 2) & 1u) << p.shift2;
+            } else {
+                words[p.chunk * 4 + p.word] |= sc << p.shift;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < BITS; ++c)
+            *reinterpret_cast<uint4*>(tbase + c * 2048) =
+                make_uint4(words[4 * c], words[4 * c + 1], words[4 * c + 2], words[4 * c + 3]);
+    }
+}
+
+// Unpack to row-major stored codes (u8, or raw bf16 words for 16-bit) and
+// row-major fp32 scale/zero. One thread per (row, group).
+template <int BITS>
+__global__ void unpack_kernel(const uint8_t* __restrict__ packed,
+                              const float* __restrict__ scale,
+                              const float* __restrict__ zero, int64_t n_out,
+                              int64_t k_in, int G, uint8_t* __restrict__ codes,
+                              float* __restrict__ scale_rm,
+                              float* __restrict__ zero_rm) {
+    const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= n_out * G) return;
+    const int64_t row = idx / G;
+    const int g = static_cast<int>(idx % G);
+    const int64_t nt = row / 128;
+    const int r = static_cast<int>(row % 128);
+    const size_t t = static_cast<size_t>(nt) * G + g;
+    const uint8_t* base = packed + t * tile_bytes(BITS) + r * 16;
+    if (scale_rm && scale) scale_rm[row * G + g] = scale[t * 128 + r];
+    if (zero_rm && zero) zero_rm[row * G + g] = zero[t * 128 + r];
+    if (!codes) return;
+    const int64_t k0 = static_cast<int64_t>(g) * 128;
+    const int cnt = static_cast<int>(k_in - k0 < 128 ? k_in - k0 : 128);
+    for (int kk = 0; kk < cnt; ++kk) {
+        if constexpr (BITS == 16) {
+            const uint16_t v = *reinterpret_cast<const uint16_t*>(base + (kk >> 3) * 2048 + (kk & 7) * 2);
+            reinterpret_cast<uint16_t*>(codes)[row * k_in + k0 + kk] = v;
+        } else {
+            const code_pos p = locate_code(BITS, kk);
+            const uint32_t* wd = reinterpret_cast<const uint32_t*>(base + p.chunk * 2048);
+            uint32_t c;
+            if constexpr (BITS == 3) {
+                const uint32_t* hd = reinterpret_cast<const uint32_t*>(base + p.chunk2 * 2048);
+                c = ((wd[p.word] >> p.shift) & 3u) | (((hd[p.word2] >> p.shift2) & 1u) << 2);
+            } else {
+                c = (wd[p.word] >> p.shift) & ((1u << BITS) - 1u);
+            }
+            codes[row * k_in + k0 + kk] = static_cast<uint8_t>(c);
+        }
+    }
+}
+
+// Dense bf16 dequant through the same per-slice arithmetic the GEMM uses.
+// One thread per (row, 32-element slice).
+template <int BITS, bool SYM>
+__global__ void dequant_kernel(const uint8_t* __restrict__ packed,
+                               const float* __restrict__ scale,
+                               const float* __restrict__ zero, int64_t n_out,
+                               int64_t k_in, int G,
+                               __nv_bfloat16* __restrict__ out) {
+    const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= n_out * G * 4) return;
+    const int slice = static_cast<int>(idx & 3);
+    const int64_t rg = idx >> 2;
+    const int64_t row = rg / G;
+    const int g = static_cast<int>(rg % G);
+    const int64_t nt = row / 128;
+    const int r = static_cast<int>(row % 128);
+    const size_t t = static_cast<size_t>(nt) * G + g;
+    const uint8_t* base = packed + t * tile_bytes(BITS) + r * 16;
+    float s = 0.f, z = 0.f;
+    if (BITS != 16) {
+        s = scale[t * 128 + r];
+        z = SYM ? 0.0f : zero[t * 128 + r];
+    }
+    uint32_t v[16];
+    dequant_slice32<BITS, SYM>(base, slice, s, z, bf16x2_splat_bits(s),
+                               bf16x2_splat_bits(z), v);
+    const int64_t k0 = static_cast<int64_t>(g) * 128 + slice * 32;
+    for (int i = 0; i < 32; ++i) {
+        if (k0 + i >= k_in) break;
+        const uint16_t h = static_cast<uint16_t>((v[i >> 1] >> (16 * (i & 1))) & 0xFFFFu);
+        reinterpret_cast<uint16_t*>(out)[row * k_in + k0 + i] = h;
+    }
+}
+
+}  // namespace
+
+// ---- launchers (called from capi.cu after argument validation) -----------
+cudaError_t launch_quant_pack(const void* w, int64_t n_out, int64_t k_in,
+                              int64_t ldw, int bits, int sym, void* packed,
+                              float* scale, float* zero, double* step64,
+                              double* zero64, cudaStream_t st) {
+    const int G = static_cast<int>(ceil_div64(k_in, 128));
+    const dim3 grid(G, static_cast<unsigned>(ceil_div64(n_out, 128)));
+    auto* wp = static_cast<const __nv_bfloat16*>(w);
+    auto* pp = static_cast<uint8_t*>(packed);
+    switch (bits) {
+        case 3: quant_pack_kernel<3><<<grid, 128, 0, st>>>(wp, n_out, k_in, ldw, G, sym, pp, scale, zero, step64, zero64); break;
+        case 4: quant_pack_kernel<4><<<grid, 128, 0, st>>>(wp, n_out, k_in, ldw, G, sym, pp, scale, zero, step64, zero64); break;
+        case 8: quant_pack_kernel<8><<<grid, 128, 0, st>>>(wp, n_out, k_in, ldw, G, sym, pp, scale, zero, step64, zero64); break;
+        case 16: quant_pack_kernel<16><<<grid, 128, 0, st>>>(wp, n_out, k_in, ldw, G, sym, pp, scale, zero, step64, zero64); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unpack(const void* packed, const float* scale,
+                          const float* zero, int64_t n_out, int64_t k_in,
+                          int bits, void* codes, float* scale_rm,
+                          float* zero_rm, cudaStream_t st) {
+    const int G = static_cast<int>(ceil_div64(k_in, 128));
+    const int64_t n = n_out * G;
+    const unsigned blocks = static_cast<unsigned>(ceil_div64(n, 256));
+    auto* pp = static_cast<const uint8_t*>(packed);
+    auto* cp = static_cast<uint8_t*>(codes);
+    switch (bits) {
+        case 3: unpack_kernel<3><<<blocks, 256, 0, st>>>(pp, scale, zero, n_out, k_in, G, cp, scale_rm, zero_rm); break;
+        case 4: unpack_kernel<4><<<blocks, 256, 0, st>>>(pp, scale, zero, n_out, k_in, G, cp, scale_rm, zero_rm); break;
+        case 8: unpack_kernel<8><<<blocks, 256, 0, st>>>(pp, scale, zero, n_out, k_in, G, cp, scale_rm, zero_rm); break;
+        case 16: unpack_kernel<16><<<blocks, 256, 0, st>>>(pp, scale, zero, n_out, k_in, G, cp, scale_rm, zero_rm); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dequant(const void* packed, const float* scale,
+                           const float* zero, int64_t n_out, int64_t k_in,
+                           int bits, int sym, void* out, cudaStream_t st) {
+    const int G = static_cast<int>(ceil_div64(k_in, 128));
+    const int64_t n = n_out * G * 4;
+    const unsigned blocks = static_cast<unsigned>(ceil_div64(n, 256));
+    auto* pp = static_cast<const uint8_t*>(packed);
+    auto* op = static_cast<__nv_bfloat16*>(out);
+#define HP_DQ(B)                                                                               \
+    if (sym) dequant_kernel<B, true><<<blocks, 256, 0, st>>>(pp, scale, zero, n_out, k_in, G, op); \
+    else dequant_kernel<B, false><<<blocks, 256, 0, st>>>(pp, scale, zero, n_out, k_in, G, op);
+    switch (bits) {
+        case 3: HP_DQ(3) break;
+        case 4: HP_DQ(4) break;
+        case 8: HP_DQ(8) break;
+        case 16: dequant_kernel<16, true><<<blocks, 256, 0, st>>>(pp, scale, zero, n_out, k_in, G, op); break;
+        default: return cudaErrorInvalidValue;
+    }
+#undef HP_DQ
+    return cudaGetLastError();
+}
+
+}  // namespace hp

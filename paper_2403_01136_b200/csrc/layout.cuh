@@ -1,0 +1,186 @@
+// Packed weight layout ("tile layout") shared by K1 (writer), K3/K4
+// (readers) and the unpack/dequant utilities. See DESIGN.md §3.
+//
+//  W [n_out × k_in], groups of 128 along k. NT = ceil(n_out/128) row tiles,
+//  G = ceil(k_in/128) groups. Tile (nt, g) holds rows nt*128 + r, r<128,
+//  and k = g*128 + kk, kk<128, in bits*2048 contiguous bytes:
+//      byte offset = ((nt*G + g)*bits + c)*2048 + r*16 + b,   c < bits
+//  i.e. `bits` chunks; chunk c holds 16 bytes for every one of the 128 rows,
+//  so a warp reading chunk c of 32 consecutive rows reads 512 contiguous
+//  bytes (one LDS.128/LDG.128 per lane, conflict-free).
+//  Scale/zero (fp32): index (nt*G + g)*128 + r.
+//
+//  Inside a row's chunk (4 little-endian u32 words w0..w3), codes are placed
+//  so that one shift + one LOP3 yields a bf16x2 pair (k, k+1) for the MMA's
+//  K-major TMEM A operand (element k in the low half):
+//   4-bit: chunk c covers kk in [32c, 32c+32); word j covers [32c+8j, +8);
+//          pair p<4 (kk0 = 32c+8j+2p): bits [4p,4p+4) = code(kk0),
+//          bits [16+4p, 20+4p) = code(kk0+1).
+//   3-bit: chunks 0/1 = low-2-bit planes of kk in [0,64) / [64,128):
+//          word j covers 16 kk; pair p<8: bits [2p,2p+2) and [16+2p,18+2p).
+//          chunk 2 = bit-2 plane: word j covers kk in [32j, 32j+32);
+//          pair p<16: bit p = code(kk0) bit 2, bit 16+p = code(kk0+1) bit 2.
+//   8-bit: chunk c covers [16c, 16c+16); word j covers [16c+4j, +4),
+//          byte i = code(kk0+i).
+//   16-bit: chunk c covers [8c, 8c+8) as bf16 in natural order.
+//  Codes are unsigned "stored" codes: asymmetric code in [0, 2^b-1];
+//  symmetric signed code q in [-hi, hi] stored as q + hi (hi = 2^(b-1)-1).
+#pragma once
+
+#include <cstdint>
+
+#ifdef __CUDACC__
+#include "sm100.cuh"
+#endif
+
+namespace hp {
+
+constexpr int kGroup = 128;
+constexpr int kTileRows = 128;
+
+__host__ __device__ __forceinline__ int64_t ceil_div64(int64_t a, int64_t b) {
+    return (a + b - 1) / b;
+}
+__host__ __device__ __forceinline__ int sym_hi(int bits) {
+    return (1 << (bits - 1)) - 1;
+}
+__host__ __device__ __forceinline__ int64_t tile_bytes(int bits) {
+    return static_cast<int64_t>(bits) * 2048;
+}
+
+// Position of code kk (0..127) of a row inside its tile for 3/4/8-bit:
+// returns chunk, word, bit offset; (3-bit returns the low-2-bit position and
+// the bit-2 position separately).
+struct code_pos {
+    int chunk, word, shift;    // main field
+    int chunk2, word2, shift2; // 3-bit high bit plane
+};
+
+__host__ __device__ __forceinline__ code_pos locate_code(int bits, int kk) {
+    code_pos p{0, 0, 0, 0, 0, 0};
+    const int pair = (kk >> 1), hi = kk & 1;
+    if (bits == 4) {
+        p.chunk = kk >> 5;
+        p.word = (kk >> 3) & 3;
+        p.shift = 4 * (pair & 3) + 16 * hi;
+    } else if (bits == 8) {
+        p.chunk = kk >> 4;
+        p.word = (kk >> 2) & 3;
+        p.shift = 8 * (kk & 3);
+    } else if (bits == 3) {
+        p.chunk = kk >> 6;
+        p.word = (kk >> 4) & 3;
+        p.shift = 2 * (pair & 7) + 16 * hi;
+        p.chunk2 = 2;
+        p.word2 = kk >> 5;
+        p.shift2 = (pair & 15) + 16 * hi;
+    }
+    return p;
+}
+
+// ---------------------------------------------------------------------------
+// Device dequant of one 32-element k slice of one row into 16 bf16x2 words
+// (element 2i in the low half of out[i]). `row_chunks` points at the row's
+// first 16-byte piece inside a tile (stride 2048 B between chunks), in
+// shared or global memory. 3/4-bit: two bf16x2 FMAs per pair, exact up to
+// the final rounding of code*scale(+zero) with the scale/zero in bf16;
+// 8-bit: fp32 arithmetic with the fp32 scale, rounded once to bf16.
+// ---------------------------------------------------------------------------
+#ifdef __CUDACC__
+
+
+// magic: bf16 128.0 in both halves; OR-ing a <=7-bit integer into the
+// mantissa gives exactly 128 + v.
+constexpr uint32_t kMagic128 = 0x43004300u;
+
+__device__ __forceinline__ uint32_t bf16x2_splat_bits(float f) {
+    uint32_t d;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %1;" : "=r"(d) : "f"(f));
+    return d;
+}
+
+// (v - off) exactly, then * s (+ z): two bf16x2 FMAs.
+template <bool SYM>
+__device__ __forceinline__ uint32_t finish_pair(uint32_t v, uint32_t negoff2,
+                                                uint32_t s2, uint32_t z2) {
+    constexpr uint32_t one2 = 0x3F803F80u;  // bf16 1.0 x2
+    uint32_t c;
+    asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(c) : "r"(v), "r"(one2), "r"(negoff2));
+    uint32_t d;
+    if (SYM) {
+        asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(c), "r"(s2), "r"(0x80008000u));
+    } else {
+        asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(c), "r"(s2), "r"(z2));
+    }
+    return d;
+}
+
+// s, z: the row's fp32 scale / zero; s2, z2: their bf16x2 splats.
+template <int BITS, bool SYM>
+__device__ __forceinline__ void dequant_slice32(const uint8_t* row_chunks,
+                                                int slice, float s, float z,
+                                                uint32_t s2, uint32_t z2,
+                                                uint32_t* out) {
+    if constexpr (BITS == 4) {
+        // bf16 of (128 + hi) / 128 negated: exact small integers
+        constexpr uint32_t negoff2 =
+            SYM ? 0xC307C307u /* -135 */ : 0xC300C300u /* -128 */;
+        const uint4 q = *reinterpret_cast<const uint4*>(row_chunks + slice * 2048);
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const uint32_t v = lop3_and_or(w[j] >> (4 * p), 0x000F000Fu, kMagic128);
+                out[4 * j + p] = finish_pair<SYM>(v, negoff2, s2, z2);
+            }
+    } else if constexpr (BITS == 3) {
+        constexpr uint32_t negoff2 =
+            SYM ? 0xC303C303u /* -131 */ : 0xC300C300u /* -128 */;
+        // slice 0..3 covers kk [32*slice, +32): low planes chunk slice/2,
+        // words 2*(slice&1), +1; high plane chunk 2, word slice.
+        const uint4 lo = *reinterpret_cast<const uint4*>(row_chunks + (slice >> 1) * 2048);
+        const uint32_t hb = *reinterpret_cast<const uint32_t*>(row_chunks + 2 * 2048 + 4 * slice);
+        const uint32_t l0 = (slice & 1) ? lo.z : lo.x;
+        const uint32_t l1 = (slice & 1) ? lo.w : lo.y;
+#pragma unroll
+        for (int p = 0; p < 16; ++p) {
+            const uint32_t lw = p < 8 ? l0 : l1;
+            const uint32_t a = lop3_and_or(lw >> (2 * (p & 7)), 0x00030003u, kMagic128);
+            const uint32_t h = (p >= 2) ? (hb >> (p - 2)) : (hb << (2 - p));
+            const uint32_t v = lop3_and_or(h, 0x00040004u, a);
+            out[p] = finish_pair<SYM>(v, negoff2, s2, z2);
+        }
+    } else if constexpr (BITS == 8) {
+        // fp32 magic 2^23: float bits 0x4B0000xx == 8388608 + xx exactly.
+        const float off = SYM ? 8388608.0f + 127.0f : 8388608.0f;
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+            const uint4 q = *reinterpret_cast<const uint4*>(row_chunks + (2 * slice + cc) * 2048);
+            const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    const float f0 = __uint_as_float(prmt(w[j], 0x4B000000u, 0x7540u + 2 * p)) - off;
+                    const float f1 = __uint_as_float(prmt(w[j], 0x4B000000u, 0x7541u + 2 * p)) - off;
+                    const float d0 = SYM ? f0 * s : __fmaf_rn(f0, s, z);
+                    const float d1 = SYM ? f1 * s : __fmaf_rn(f1, s, z);
+                    out[cc * 8 + 2 * j + p] = pack_bf16x2(d0, d1);
+                }
+        }
+    } else {  // 16-bit passthrough
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+            const uint4 q = *reinterpret_cast<const uint4*>(row_chunks + (4 * slice + cc) * 2048);
+            out[4 * cc + 0] = q.x;
+            out[4 * cc + 1] = q.y;
+            out[4 * cc + 2] = q.z;
+            out[4 * cc + 3] = q.w;
+        }
+    }
+}
+
+#endif  // __CUDACC__
+
+}  // namespace hp
