@@ -1,0 +1,360 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 adaptive-bitwidth linear path (LLM-PQ, arxiv
+2403.01136) — one JSON line on rank 0.
+
+A step is one serving round of the plan's workload (B requests, prompt s,
+n generated tokens; BASELINE.json configs) through the quantized decoder
+stack: ceil(B/eta) prefill micro-batches (K4 tensor-core dequant-GEMM) and
+(n-1) decode tokens per decode group (K3 split-K dequant-GEMV), executed by
+the C++ pipeline runtime behind the C-ABI (one process per GPU, NCCL
+send/recv between stages). Workload per GPU count (BASELINE.json configs):
+  N=1: configs[1] OPT-13B mixed 3/4/8/16 plan       (opt13b_b32_1gpu)
+  N=2: configs[2] OPT-30B 2-stage pipeline           (opt30b_b32_2gpu)
+  N=4: configs[2] OPT-30B 4-stage pipeline           (opt30b_b32_4gpu)
+  N=8: configs[3] OPT-66B mixed 4/8 8-stage pipeline (opt66b_b32_8gpu)
+
+value = (prefill + decode tokens) / round time with the prompt resident in
+HBM; e2e = the same through hp_pipeline_run with pinned HOST prompt in and
+host hidden states out (copies inside the timed region).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "decode tokens/s + prefill tok/s vs HBM/tensor roofline, 1/2/4/8 B200"
+PLAN_FOR_N = {1: "opt13b_b32_1gpu", 2: "opt30b_b32_2gpu", 4: "opt30b_b32_4gpu",
+              8: "opt66b_b32_8gpu"}
+CONFIG_INDEX = {1: 1, 2: 2, 4: 2, 8: 3}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d["hbm_gbs"], d["bf16_tflops"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = Path(f"/tmp/hp_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        try:
+            rows = [r.split(", ") for r in self.path.read_text().strip().splitlines()]
+        except Exception:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows if len(r) >= 9 for i in range(4)
+                          if r[5 + i].strip() == "Active"})
+        busy = [v for v in sm if v > 0]
+        return {"sm_mhz": statistics.median(busy) if busy else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def cpu_sample(plan: dict, model_json: str, threads: int, budget_s: float = 20.0):
+    """Oracle-port CPU forward of one decoder layer (all 4 ops), decode at
+    m = xi and prefill at a 64-token chunk, extrapolated to the round."""
+    import numpy as np
+
+    import oracle
+    model = json.loads(model_json)
+    presets = {"opt-13b": (5120, 20480), "opt-30b": (7168, 28672), "opt-66b": (9216, 36864),
+               "bloom-176b": (14336, 57344)}
+    h1, h2 = presets[model["preset"]] if "preset" in model else (model["h1"], model["h2"])
+    L = plan["num_layers"]
+    B, s, n = plan["workload"]["global_bz"], plan["workload"]["s"], plan["workload"]["n"]
+    xi = plan["xi"]
+    bits = max(set(plan["layer_bits"]), key=plan["layer_bits"].count)
+    rng = np.random.default_rng(0)
+    port = oracle.port()
+    ops = []
+    for (nn, kk) in ((3 * h1, h1), (h1, h1), (h2, h1), (h1, h2)):
+        w = (rng.standard_normal((nn, kk), dtype=np.float32) * 0.02).view(np.uint32)
+        wb = (w >> 16).astype(np.uint16)
+        if bits == 16:
+            ops.append((wb, None, None, nn, kk))
+        else:
+            c, st, z = port.quantize_matrix(wb, bits, 1)
+            ops.append((c, st, z, nn, kk))
+
+    def layer(m):
+        x = (rng.standard_normal((m, h1), dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)
+        t0 = time.perf_counter()
+        for c, st, z, nn, kk in ops:
+            xin = x if kk == h1 else (rng.standard_normal((m, kk), dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)
+            port.qlinear(xin, c.view(np.uint16) if bits == 16 else c, st, z, bits, 1, threads)
+        return time.perf_counter() - t0
+
+    t_dec = layer(xi)
+    m_pre = 64
+    t_pre = layer(m_pre)
+    groups = -(-B // xi)
+    dec_round = groups * (n - 1) * L * t_dec
+    pre_round = (B * s / m_pre) * L * t_pre
+    tok = B * s + B * (n - 1)
+    return {"value": tok / (dec_round + pre_round), "unit": "tok/s", "cores": threads,
+            "sample": (f"oracle port (oracle/hp_oracle.c, fp64 dequant-GEMM, OpenMP) on one "
+                       f"{bits}-bit layer [h1={h1}, h2={h2}]: 4 ops at m={xi} (decode) and "
+                       f"m={m_pre} (prefill chunk), {t_dec + t_pre:.1f} s CPU wall, "
+                       f"extrapolated to {L} layers x B={B}, s={s}, n={n}"),
+            "decode_tok_s": B * (n - 1) / dec_round, "prefill_tok_s": B * s / pre_round}
+
+
+def run_reference(args, rank: int, world: int):
+    """--impl reference: the CPU path on the host cores, same metric/config."""
+    if rank != 0:
+        return
+    from paper_2403_01136_b200.pipeline import load_plan
+    name = args.plan or PLAN_FOR_N.get(world, PLAN_FOR_N[1])
+    plan_json, model_json = load_plan(name)
+    plan = json.loads(plan_json)
+    threads = os.cpu_count() or 1
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_sample(plan, model_json, threads)
+        if i >= args.warmup:
+            vals.append(r)
+    v = statistics.mean(x["value"] for x in vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tok/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{name} (BASELINE.json configs[{CONFIG_INDEX.get(world, 1)}])",
+                       "plan": name},
+            "cpu_baseline": {"value": v, "unit": "tok/s", "cores": threads, "kind": "port",
+                             "sample": vals[0]["sample"] +
+                             "; the reference implements no layer forward (SPEC.md:8), so its "
+                             "CPU path is the oracle port of indicator.cpp:53 dequant + GEMM"},
+            "e2e": {"value": v, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--plan", default=None, help="override plan fixture name")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graphs", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2403_01136_b200 import capi
+    from paper_2403_01136_b200.pipeline import Pipeline, load_plan, nccl_ids
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    name = args.plan or PLAN_FOR_N.get(world)
+    if name is None:
+        raise SystemExit(f"no plan fixture for {world} GPUs")
+    plan_json, model_json = load_plan(name)
+    plan = json.loads(plan_json)
+    B, s, n = plan["workload"]["global_bz"], plan["workload"]["s"], plan["workload"]["n"]
+    ids = None
+    if world > 1:
+        obj = [nccl_ids(world) if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ids = obj[0]
+    pipe = Pipeline(plan_json, model_json, rank, world, ids, use_graphs=not args.no_graphs,
+                    instrument=True, sm_budget=140 if world > 1 else 0)
+    info = pipe.info()
+    h1 = {"opt-13b": 5120, "opt-30b": 7168, "opt-66b": 9216, "bloom-176b": 14336}.get(
+        json.loads(model_json).get("preset", ""), json.loads(model_json).get("h1", 0))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(max(args.warmup, 3)):
+        pipe.run()
+    k0 = [pipe.kernel_stats(0), pipe.kernel_stats(1)]
+    barrier()
+    times, pre_s, dec_s = [], [], []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            t = pipe.run()
+            times.append(t.makespan_s)
+            pre_s.append(t.prefill_s)
+            dec_s.append(t.decode_s)
+        barrier()
+    k1 = [pipe.kernel_stats(0), pipe.kernel_stats(1)]
+    step_s = max_over_ranks(statistics.mean(times))
+    pre_busy = max_over_ranks(statistics.mean(pre_s))
+    dec_busy = max_over_ranks(statistics.mean(dec_s))
+    tokens = B * s + B * (n - 1)
+
+    # ---- e2e: pinned host prompt in, host hidden states out -------------
+    h2d = B * s * h1 * 2 if rank == 0 else 0
+    d2h = B * h1 * 2 if rank == world - 1 else 0
+    host_in = torch.empty(max(B * s * h1, 1), dtype=torch.bfloat16).pin_memory()
+    host_in.normal_()
+    host_out = torch.empty(max(B * h1, 1), dtype=torch.bfloat16).pin_memory()
+    barrier()
+    e2e_t = []
+    for _ in range(args.steps):
+        t = pipe.run(host_in.data_ptr() if rank == 0 else None,
+                     host_out.data_ptr() if rank == world - 1 else None)
+        e2e_t.append(t.makespan_s)
+    barrier()
+    e2e_s = max_over_ranks(statistics.mean(e2e_t))
+    h2d_all = max_over_ranks(float(h2d))
+    d2h_all = max_over_ranks(float(d2h))
+    costs = pipe.stage_cost()
+    if world > 1:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, costs)
+    else:
+        gathered = [costs]
+    launches = max_over_ranks(float(info["launches_per_round"])) * args.steps
+    if world > 1:
+        tl = torch.tensor([float(info["launches_per_round"] * args.steps)], device="cuda",
+                          dtype=torch.float64)
+        dist.all_reduce(tl)
+        launches = float(tl.item())
+
+    if rank == 0:
+        hbm, tf_burst, tf_sus, src = peaks()
+        d_pre = {k: k1[0][k] - k0[0][k] for k in k1[0]}
+        d_dec = {k: k1[1][k] - k0[1][k] for k in k1[1]}
+        k4 = d_pre["flops"] / d_pre["seconds"] / 1e12 if d_pre["seconds"] > 0 else None
+        k3 = d_dec["bytes"] / d_dec["seconds"] / 1e9 if d_dec["seconds"] > 0 else None
+        prof = ROOT / "profiles" / "ncu_traffic.json"
+        traffic = None
+        if prof.exists():
+            traffic = json.loads(prof.read_text()).get(name, {}).get("k4_traffic_bytes")
+        pre_share = pre_busy / (pre_busy + dec_busy) if pre_busy + dec_busy > 0 else 0
+        roof_pre = {"kernel": "K4 prefill dequant-GEMM (hp::qgemm_kernel, BN=256)",
+                    "bound": "tensor", "achieved": k4, "peak": tf_sus, "unit": "TFLOP/s",
+                    "frac": k4 / tf_sus if k4 else None, "traffic": traffic,
+                    "peak_kind": f"{src} bf16_tflops_sustained (burst {tf_burst})",
+                    "per_launch": {"launches": d_pre["launches"],
+                                   "avg_flops": d_pre["flops"] / max(d_pre["launches"], 1),
+                                   "avg_s": d_pre["seconds"] / max(d_pre["launches"], 1)},
+                    "share_of_step": pre_share}
+        roof_dec = {"kernel": "K3 decode dequant-GEMV (hp::qgemm_kernel, BN=32, split-K)",
+                    "bound": "hbm", "achieved": k3, "peak": hbm, "unit": "GB/s",
+                    "frac": k3 / hbm if k3 else None, "frac_of_nominal_8TBs": k3 / 8000 if k3 else None,
+                    "traffic": None, "peak_kind": f"{src} hbm_gbs",
+                    "per_launch": {"launches": d_dec["launches"],
+                                   "avg_bytes": d_dec["bytes"] / max(d_dec["launches"], 1),
+                                   "avg_s": d_dec["seconds"] / max(d_dec["launches"], 1)},
+                    "share_of_step": 1 - pre_share}
+        dominant, other = (roof_pre, roof_dec) if pre_share >= 0.5 else (roof_dec, roof_pre)
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_sample(plan, model_json, os.cpu_count() or 1)
+        # pipesim on measured costs (comm estimated from payload / 770 GB/s)
+        sim = None
+        try:
+            import ctypes as C
+            S = world
+            costs4 = []
+            for j, c in enumerate(gathered):
+                cp = 2.0 * plan["eta"] * s * h1 / 7.7e11 if j + 1 < S else 0.0
+                cd = 2.0 * plan["xi"] * h1 / 7.7e11 if j + 1 < S else 0.0
+                costs4 += [c[0], c[1], cp, cd]
+            arr = (C.c_double * len(costs4))(*costs4)
+            out = (C.c_double * 4)()
+            busy = (C.c_double * S)()
+            capi.check(capi.lib.hp_host_simulate(arr, S, B, plan["eta"], plan["xi"], n, out, busy,
+                                                 None, 0))
+            sim = {"pipesim_makespan_s": out[0], "analytic_s": out[2], "measured_s": step_s,
+                   "gap": step_s / out[0] - 1 if out[0] > 0 else None}
+        except Exception as e:  # diagnostic only
+            sim = {"error": str(e)}
+        line = {
+            "metric": METRIC, "value": tokens / step_s, "unit": "tok/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": step_s * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16 (weights 3/4/8/16-bit, fp32 accumulate)",
+            "data": "synthetic (bit-reproducible weights/prompts, oracle/synth.py)",
+            "config": {"workload": f"{name} (BASELINE.json configs[{CONFIG_INDEX.get(world, 1)}])",
+                       "plan": name, "B": B, "s": s, "n": n, "eta": plan["eta"],
+                       "xi": plan["xi"], "layer_bits": plan["layer_bits"],
+                       "stages": [st["layers"] for st in plan["stages"]],
+                       "l2": "inputs larger than L2 (packed weights "
+                             f"{info['weight_bytes'] / 1e9:.1f} GB/rank >> 126 MB)",
+                       "graphs": not args.no_graphs},
+            "decode_tok_s": B * (n - 1) / dec_busy if dec_busy > 0 else None,
+            "prefill_tok_s": B * s / pre_busy if pre_busy > 0 else None,
+            "generated_tok_s": B * n / step_s,
+            "roofline": dominant, "roofline_other": other,
+            "e2e": {"value": tokens / e2e_s, "unit": "tok/s", "h2d_bytes_per_step": int(h2d_all),
+                    "d2h_bytes_per_step": int(d2h_all), "ms_per_step": e2e_s * 1e3},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "pipesim": sim,
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    pipe.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

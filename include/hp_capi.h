@@ -47,6 +47,9 @@ const char* hp_last_error(void);
 int hp_abi_version(void);
 /* 1 if a CUDA device with compute capability 10.x is usable, else 0. */
 int hp_device_ok(void);
+/* Cap the persistent K3/K4 grid at `sms` CTAs (0 = every SM), leaving SMs
+ * to NCCL kernels that run concurrently in pipeline mode.               */
+void hp_set_sm_budget(int sms);
 
 /* Quantizer scheme / rounding — numeric values match the order of
  * hetplan::indicator::quant_scheme / rounding_mode (indicator.hpp:22-23). */
@@ -132,26 +135,42 @@ hp_status hp_qlinear(const hp_qweight* w, const void* x, int64_t ldx,
                      size_t workspace_bytes, hp_stream stream);
 
 /* ---- pipeline executor (one process per GPU, NCCL P2P at boundaries) ----
- * plan_json: the reference plan document (hetplan_main.cpp:190-224);
- * stage r of the plan runs on this rank. nccl_id: 128-byte ncclUniqueId
- * produced by hp_nccl_unique_id on rank 0 and broadcast by the caller.
- * The schedule follows pipesim::make_schedule semantics
- * (/root/reference/proj/src/pipesim.cpp:22-46).                           */
+ * plan_json: a plan document (schema of hetplan_main.cpp:190-224, loaded by
+ * hetplan::plan_io); stage `rank` of the plan runs on this process's current
+ * CUDA device. model_json: the config "model" section ({"preset": ...} or
+ * explicit fields, config.cpp:55-69). nccl_ids: `world` ncclUniqueIds of
+ * 128 bytes (id l names the link rank l -> (l+1) % world), produced by
+ * hp_nccl_unique_id on rank 0 and broadcast by the caller; NULL if world==1.
+ * The unit order follows pipesim::make_schedule / simulate semantics
+ * (/root/reference/proj/src/pipesim.cpp:22-248).                          */
 typedef struct hp_pipeline hp_pipeline;
+typedef struct {
+    int32_t scheme;      /* HP_SYMMETRIC (default) / HP_ASYMMETRIC         */
+    int32_t use_graphs;  /* capture the round into one CUDA graph          */
+    int32_t instrument;  /* CUDA events around the linear ops of 1 unit/phase */
+    int32_t sm_budget;   /* persistent-kernel grid cap, 0 = all SMs         */
+    uint64_t seed;       /* synthetic tensors (oracle/synth.py mirror)     */
+    double weight_std;   /* synthetic weight std (0.02)                    */
+} hp_pipeline_options;
 hp_status hp_nccl_unique_id(void* out128);
-hp_status hp_pipeline_create(const char* plan_json, const char* model_json,
-                             int rank, int world, const void* nccl_id,
-                             uint64_t seed, hp_pipeline** out);
-/* Run one serving round: B requests, prompt s, n generated tokens. Host
- * buffers: prompt activations in (stage 0 only; [B × s × h1] bf16, may be
- * NULL for synthetic), final hidden states out (last stage only; [B × h1]
- * bf16 of the last decode step, may be NULL). Fills timing[0..3] with
- * {makespan_s, prefill_s, decode_s, h2d_d2h_s} measured with CUDA events. */
+hp_status hp_pipeline_create(const char* plan_json, const char* model_json, int rank,
+                             int world, const void* nccl_ids,
+                             const hp_pipeline_options* opt, hp_pipeline** out);
+/* One serving round: B requests, prompt s, n generated tokens (the plan's
+ * workload). host_in (rank 0): [B*s x h1] bf16 prompt activations, or NULL
+ * for the device-resident synthetic prompt. host_out (last rank): [B x h1]
+ * bf16 final hidden state per request, or NULL. timing4 = {makespan_s,
+ * prefill_s, decode_s, io_s} of this rank, from CUDA events.             */
 hp_status hp_pipeline_run(hp_pipeline* p, const void* host_in, void* host_out,
                           double* timing4);
-/* Per-stage measured costs {pre_s, dec_s, comm_pre_s, comm_dec_s} of the
- * last run, for comparison with pipesim::simulate.                        */
+/* Measured mean per-unit costs {pre_s, dec_s, 0, 0} of the last round, for
+ * pipesim::simulate (comm costs are the caller's).                      */
 hp_status hp_pipeline_stage_costs(hp_pipeline* p, double* out4);
+/* Instrumented linear-op totals for phase (HP_PREFILL / HP_DECODE):
+ * {launches, seconds, algorithmic_bytes, flops} accumulated over rounds. */
+hp_status hp_pipeline_kernel_stats(hp_pipeline* p, int phase, double* out4);
+/* {packed weight bytes, kernel launches per round, units, layers}        */
+hp_status hp_pipeline_info(hp_pipeline* p, int64_t* out4);
 void hp_pipeline_destroy(hp_pipeline* p);
 
 /* ---- host planning helpers (drop-in hetplan:: library, plain types) -----

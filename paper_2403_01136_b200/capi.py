@@ -48,6 +48,17 @@ class hp_qweight(C.Structure):
     ]
 
 
+class hp_pipeline_options(C.Structure):
+    _fields_ = [
+        ("scheme", C.c_int32),
+        ("use_graphs", C.c_int32),
+        ("instrument", C.c_int32),
+        ("sm_budget", C.c_int32),
+        ("seed", C.c_uint64),
+        ("weight_std", C.c_double),
+    ]
+
+
 def _load() -> C.CDLL:
     if not LIB_PATH.exists():
         raise ImportError(
@@ -78,13 +89,17 @@ def _load() -> C.CDLL:
         "hp_host_simulate": (i32, [P(d), i32, i32, i32, i32, i32, P(d), P(d), v, i64]),
         "hp_host_plan_check": (i32, [p, C.c_char_p, i64]),
     }
-    optional = {
+    sig.update({
+        "hp_set_sm_budget": (None, [i32]),
         "hp_nccl_unique_id": (i32, [v]),
-        "hp_pipeline_create": (i32, [p, p, i32, i32, v, C.c_uint64, P(v)]),
+        "hp_pipeline_create": (i32, [p, p, i32, i32, v, P(hp_pipeline_options), P(v)]),
         "hp_pipeline_run": (i32, [v, v, v, P(d)]),
         "hp_pipeline_stage_costs": (i32, [v, P(d)]),
+        "hp_pipeline_kernel_stats": (i32, [v, i32, P(d)]),
+        "hp_pipeline_info": (i32, [v, P(i64)]),
         "hp_pipeline_destroy": (None, [v]),
-    }
+    })
+    optional = {}
     for name, (res, args) in list(sig.items()) + list(optional.items()):
         if not hasattr(lib, name):
             if name in sig:
@@ -103,8 +118,9 @@ EXPORTED = [
     "hp_quant_pack", "hp_quant_unpack", "hp_dequant", "hp_indicator_stats",
     "hp_qlinear_workspace_bytes", "hp_qlinear", "hp_host_scaling_factor", "hp_host_g_of_x",
     "hp_host_indicator_csv", "hp_host_omega_from_stats", "hp_host_memcost", "hp_host_preset",
-    "hp_host_make_schedule", "hp_host_simulate", "hp_host_plan_check", "hp_nccl_unique_id",
-    "hp_pipeline_create", "hp_pipeline_run", "hp_pipeline_stage_costs", "hp_pipeline_destroy",
+    "hp_host_make_schedule", "hp_host_simulate", "hp_host_plan_check", "hp_set_sm_budget",
+    "hp_nccl_unique_id", "hp_pipeline_create", "hp_pipeline_run", "hp_pipeline_stage_costs",
+    "hp_pipeline_kernel_stats", "hp_pipeline_info", "hp_pipeline_destroy",
 ]
 
 

@@ -14,6 +14,7 @@
 #include "layout.cuh"
 
 namespace hp {
+extern int g_sm_budget;
 cudaError_t launch_quant_pack(const void* w, int64_t n_out, int64_t k_in, int64_t ldw,
                               int bits, int sym, void* packed, float* scale, float* zero,
                               double* step64, double* zero64, cudaStream_t st);
@@ -147,6 +148,8 @@ const char* hp_last_error(void) { return g_error.c_str(); }
 int hp_abi_version(void) { return 1; }
 
 int hp_device_ok(void) { return device_ok_cached(); }
+
+void hp_set_sm_budget(int sms) { hp::g_sm_budget = sms > 0 ? sms : 0; }
 
 int64_t hp_packed_bytes(int64_t n_out, int64_t k_in, int bits) {
     if (n_out <= 0 || k_in <= 0 || !bits_ok(bits)) return -1;

@@ -1,0 +1,121 @@
+// Glue kernels of the decoder stack around the quantized linear ops — NOT
+// the graded hot path (SURVEY §8f rank 2 lists full layer glue as "next"):
+//   * hp_synth_bf16: bit-reproducible synthetic tensors (weights, norm
+//     params, prompts). Mirrors oracle/synth.py exactly: Irwin-Hall(4) of
+//     splitmix64 draws, one fp64 multiply + add, fp32 then bf16 RNE.
+//   * layernorm_bf16: OPT pre-LN (gain/bias), fp32 statistics.
+//   * gather_rows: last-position rows of each request (prefill -> decode).
+#include <cuda_bf16.h>
+#include <cstdint>
+
+namespace hp {
+
+namespace {
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__global__ void synth_kernel(__nv_bfloat16* __restrict__ out, int64_t n, uint64_t seed,
+                             double mean, double scale) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t r1 = splitmix64(seed ^ (static_cast<uint64_t>(i) << 1));
+        const uint64_t r2 = splitmix64(seed ^ ((static_cast<uint64_t>(i) << 1) | 1ull));
+        const uint64_t tot = (r1 & 0xFFFFFFFFull) + (r1 >> 32) + (r2 & 0xFFFFFFFFull) + (r2 >> 32);
+        const double v = static_cast<double>(static_cast<int64_t>(tot) - (int64_t(1) << 33));
+        const float f = __double2float_rn(__dadd_rn(mean, __dmul_rn(v, scale)));
+        out[i] = __float2bfloat16_rn(f);
+    }
+}
+
+// One CTA per row; fp32 two-pass statistics over the row held in registers.
+template <int kThreads>
+__global__ void __launch_bounds__(kThreads)
+    layernorm_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx, int h,
+                     const __nv_bfloat16* __restrict__ gamma, const __nv_bfloat16* __restrict__ beta,
+                     __nv_bfloat16* __restrict__ y, int64_t ldy) {
+    constexpr int kMaxPer = 64;  // h <= 64 * kThreads
+    __shared__ float red[kThreads / 32];
+    const __nv_bfloat16* xr = x + blockIdx.x * ldx;
+    __nv_bfloat16* yr = y + blockIdx.x * ldy;
+    float v[kMaxPer];
+    float s = 0.f;
+    int cnt = 0;
+#pragma unroll
+    for (int j = 0; j < kMaxPer; ++j) {
+        const int c = threadIdx.x + j * kThreads;
+        v[j] = c < h ? __bfloat162float(xr[c]) : 0.f;
+        s += v[j];
+        cnt += c < h;
+    }
+    auto block_sum = [&](float a) {
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) a += __shfl_xor_sync(0xffffffffu, a, d);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+        __syncthreads();
+        float t = 0.f;
+#pragma unroll
+        for (int i = 0; i < kThreads / 32; ++i) t += red[i];
+        __syncthreads();
+        return t;
+    };
+    const float mean = block_sum(s) / static_cast<float>(h);
+    float q = 0.f;
+#pragma unroll
+    for (int j = 0; j < kMaxPer; ++j) {
+        const int c = threadIdx.x + j * kThreads;
+        const float d = c < h ? v[j] - mean : 0.f;
+        q += d * d;
+    }
+    const float rstd = rsqrtf(block_sum(q) / static_cast<float>(h) + 1e-5f);
+#pragma unroll
+    for (int j = 0; j < kMaxPer; ++j) {
+        const int c = threadIdx.x + j * kThreads;
+        if (c < h)
+            yr[c] = __float2bfloat16_rn((v[j] - mean) * rstd * __bfloat162float(gamma[c]) +
+                                        __bfloat162float(beta[c]));
+    }
+    (void)cnt;
+}
+
+// dst[i] = src[(i * stride + offset)] rows of width h (bf16), i < rows
+__global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ src, int64_t lds,
+                                   int64_t stride, int64_t offset, int rows, int h,
+                                   __nv_bfloat16* __restrict__ dst, int64_t ldd) {
+    const int r = blockIdx.x;
+    const __nv_bfloat16* s = src + (static_cast<int64_t>(r) * stride + offset) * lds;
+    for (int c = threadIdx.x; c < h; c += blockDim.x) dst[r * ldd + c] = s[c];
+}
+
+}  // namespace
+
+cudaError_t launch_synth(void* out, int64_t n, uint64_t seed, double mean, double std_,
+                         cudaStream_t st) {
+    const double scale = std_ * (1.7320508075688772 * 2.3283064365386963e-10);
+    const int64_t blocks64 = (n + 255) / 256;
+    const unsigned blocks = static_cast<unsigned>(blocks64 < 148 * 64 ? blocks64 : 148 * 64);
+    synth_kernel<<<blocks, 256, 0, st>>>(static_cast<__nv_bfloat16*>(out), n, seed, mean, scale);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_layernorm(const void* x, int64_t ldx, int64_t rows, int h, const void* gamma,
+                             const void* beta, void* y, int64_t ldy, cudaStream_t st) {
+    if (h > 64 * 256) return cudaErrorInvalidValue;
+    layernorm_kernel<256><<<static_cast<unsigned>(rows), 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(x), ldx, h, static_cast<const __nv_bfloat16*>(gamma),
+        static_cast<const __nv_bfloat16*>(beta), static_cast<__nv_bfloat16*>(y), ldy);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather_rows(const void* src, int64_t lds, int64_t stride, int64_t offset,
+                               int rows, int h, void* dst, int64_t ldd, cudaStream_t st) {
+    gather_rows_kernel<<<rows, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(src), lds, stride,
+                                             offset, rows, h, static_cast<__nv_bfloat16*>(dst), ldd);
+    return cudaGetLastError();
+}
+
+}  // namespace hp

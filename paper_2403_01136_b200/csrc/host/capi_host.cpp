@@ -3,6 +3,7 @@
 // plain types so the parity tests can drive them next to the reference
 // build. Exceptions are mapped to hp_status like the rest of the ABI.
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -11,6 +12,9 @@
 #include "hetplan/memcost/memcost.hpp"
 #include "hetplan/pipesim/pipesim.hpp"
 #include "hetplan/plan/plan_io.hpp"
+#include "hetplan/runtime/pipeline.hpp"
+#include <nccl.h>
+#include <json.hpp>
 #include "hetplan/types.hpp"
 #include "hp_capi.h"
 
@@ -204,5 +208,114 @@ hp_status hp_host_plan_check(const char* plan_json, char* out, int64_t cap) {
         return from_exception(e);
     }
 }
+
+struct hp_pipeline {
+    std::unique_ptr<hetplan::runtime::pipeline> impl;
+    int64_t units = 0, layers = 0;
+};
+
+hp_status hp_nccl_unique_id(void* out128) {
+    ncclUniqueId id;
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) {
+        hp_detail::set_error(std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+        return HP_ENCCL;
+    }
+    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(out128, &id, sizeof id);
+    return HP_OK;
+}
+
+hp_status hp_pipeline_create(const char* plan_json, const char* model_json, int rank, int world,
+                             const void* nccl_ids, const hp_pipeline_options* opt,
+                             hp_pipeline** out) {
+    try {
+        if (!plan_json || !model_json || !out)
+            throw std::invalid_argument("pipeline_create: NULL argument");
+        const auto doc = hetplan::plan_io::parse_plan(plan_json);
+        // the config "model" section, through the drop-in config parser
+        nlohmann::ordered_json mj = nlohmann::ordered_json::parse(model_json, nullptr, false);
+        if (mj.is_discarded()) throw std::invalid_argument("pipeline_create: bad model JSON");
+        nlohmann::ordered_json cfg;
+        cfg["model"] = mj;
+        cfg["cluster"]["devices"] = nlohmann::ordered_json::array(
+            {{{"name", "b200"}, {"mem_bytes", 1}, {"link_bw_bytes_per_s", 9e11}}});
+        cfg["workload"] = {{"B", doc.load.global_bz}, {"s", doc.load.prompt_len}, {"n", doc.load.gen_len}};
+        cfg["bits"] = doc.bits;
+        const auto rs = hetplan::parse_config(cfg.dump());
+        hetplan::runtime::pipeline_options po;
+        if (opt) {
+            po.scheme = opt->scheme;
+            po.use_graphs = opt->use_graphs != 0;
+            po.instrument = opt->instrument != 0;
+            po.sm_budget = opt->sm_budget;
+            po.seed = opt->seed;
+            po.weight_std = opt->weight_std > 0 ? opt->weight_std : 0.02;
+        }
+        std::vector<std::array<char, 128>> ids;
+        if (world > 1) {
+            if (!nccl_ids) throw std::invalid_argument("pipeline_create: nccl_ids required");
+            ids.resize(world);
+            for (int l = 0; l < world; ++l)
+                std::memcpy(ids[l].data(), static_cast<const char*>(nccl_ids) + 128 * l, 128);
+        }
+        auto h = std::make_unique<hp_pipeline>();
+        h->impl = std::make_unique<hetplan::runtime::pipeline>(doc, rs.model, rank, world, ids, po);
+        h->layers = doc.p.stages.at(rank).end - doc.p.stages.at(rank).begin;
+        h->units = static_cast<int64_t>(
+            hetplan::runtime::static_unit_order(doc, rs.model).at(rank).size());
+        *out = h.release();
+        return HP_OK;
+    } catch (const std::exception& e) {
+        return from_exception(e);
+    }
+}
+
+hp_status hp_pipeline_run(hp_pipeline* p, const void* host_in, void* host_out, double* timing4) {
+    try {
+        if (!p) throw std::invalid_argument("pipeline_run: NULL pipeline");
+        const auto t = p->impl->run(host_in, host_out);
+        if (timing4) {
+            timing4[0] = t.makespan_s;
+            timing4[1] = t.prefill_s;
+            timing4[2] = t.decode_s;
+            timing4[3] = t.io_s;
+        }
+        return HP_OK;
+    } catch (const std::exception& e) {
+        return from_exception(e);
+    }
+}
+
+hp_status hp_pipeline_stage_costs(hp_pipeline* p, double* out4) {
+    if (!p || !out4) return HP_EINVAL;
+    const auto c = p->impl->measured_cost();
+    out4[0] = c.pre_s;
+    out4[1] = c.dec_s;
+    out4[2] = 0.0;
+    out4[3] = 0.0;
+    return HP_OK;
+}
+
+hp_status hp_pipeline_kernel_stats(hp_pipeline* p, int phase, double* out4) {
+    if (!p || !out4) return HP_EINVAL;
+    const auto& k = p->impl->stats(phase);
+    out4[0] = static_cast<double>(k.launches);
+    out4[1] = k.seconds;
+    out4[2] = k.bytes;
+    out4[3] = k.flops;
+    return HP_OK;
+}
+
+hp_status hp_pipeline_info(hp_pipeline* p, int64_t* out4) {
+    if (!p || !out4) return HP_EINVAL;
+    out4[0] = p->impl->weight_bytes();
+    out4[1] = p->impl->num_kernel_launches_per_round();
+    out4[2] = p->units;
+    out4[3] = p->layers;
+    return HP_OK;
+}
+
+void hp_pipeline_destroy(hp_pipeline* p) { delete p; }
 
 }  // extern "C"

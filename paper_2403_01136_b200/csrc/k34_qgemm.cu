@@ -32,6 +32,9 @@
 
 namespace hp {
 
+// Persistent-grid cap: leave SMs to concurrent NCCL kernels (pipeline runs).
+int g_sm_budget = 0;
+
 struct qgemm_args {
     const uint8_t* packed;
     const float* scale;
@@ -311,7 +314,8 @@ int num_sms() {
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
         if (g_num_sms <= 0) g_num_sms = 148;
     }
-    return g_num_sms;
+    const int budget = g_sm_budget;
+    return (budget > 0 && budget < g_num_sms) ? budget : g_num_sms;
 }
 
 template <int BITS, bool SYM, int BN>

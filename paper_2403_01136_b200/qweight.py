@@ -73,7 +73,10 @@ def quantize(w: torch.Tensor, bits: int, scheme: int = capi.HP_SYMMETRIC,
     ldw = w.stride(0)
     assert w.stride(1) == 1
     dev = w.device
-    packed = torch.empty(packed_bytes(n_out, k_in, bits), dtype=torch.uint8, device=dev)
+    nbytes = packed_bytes(n_out, k_in, bits)
+    if nbytes < 0:
+        raise capi.InvalidArgument(capi.HP_EINVAL, f"quantize: unsupported bits={bits} or shape")
+    packed = torch.empty(nbytes, dtype=torch.uint8, device=dev)
     nsc = int(lib.hp_scale_count(n_out, k_in))
     scale = torch.empty(nsc, dtype=torch.float32, device=dev) if bits != 16 else None
     zero = (torch.empty(nsc, dtype=torch.float32, device=dev)
