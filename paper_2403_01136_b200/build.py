@@ -42,7 +42,7 @@ def _compile(src: Path, verbose: bool) -> Path:
         return obj
     if src.suffix == ".cu":
         cmd = [str(CUDA / "bin" / "nvcc"), *GENCODE, "-O3", "-lineinfo", "-std=c++17",
-               "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-Xptxas", "-v",
+               "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-Xptxas", "-v", *os.environ.get("HP_NVCC_EXTRA", "").split(),
                *INCLUDES, "-c", str(src), "-o", str(obj)]
     else:
         cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-Wall", "-Wno-unused-function",

@@ -11,7 +11,7 @@ import os
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libhetplan_b200.so"
+LIB_PATH = Path(os.environ.get("HP_LIB_PATH", _PKG / "libhetplan_b200.so"))
 
 HP_OK, HP_EINTERNAL, HP_EINVAL, HP_EINFEASIBLE, HP_ETIMEOUT, HP_ECUDA, HP_ENCCL = 0, 1, 2, 3, 4, 5, 6
 HP_ASYMMETRIC, HP_SYMMETRIC = 0, 1

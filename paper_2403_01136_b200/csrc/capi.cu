@@ -15,6 +15,7 @@
 
 namespace hp {
 extern int g_sm_budget;
+extern unsigned long long* g_trace;
 cudaError_t launch_quant_pack(const void* w, int64_t n_out, int64_t k_in, int64_t ldw,
                               int bits, int sym, void* packed, float* scale, float* zero,
                               double* step64, double* zero64, cudaStream_t st);
@@ -31,8 +32,11 @@ cudaError_t launch_stats(const void* w, int64_t n_out, int64_t k_in, int64_t ldw
 struct qgemm_plan {
     int bn, mt, splits, gps, units, grid;
     size_t workspace;
+    int stream_k, maxseg;
+    int64_t total;
 };
 qgemm_plan plan_qgemm(int64_t n_out, int64_t k_in, int64_t m, int phase);
+int groups_per_stage(int bn);
 cudaError_t launch_qgemm(const CUtensorMap& map, const qgemm_plan& p, int bits, bool sym,
                          const void* packed, const float* scale, const float* zero,
                          int64_t n_out, int64_t k_in, int64_t m, void* y, int64_t ldy,
@@ -105,17 +109,21 @@ encode_fn get_encode() {
     return fn;
 }
 
-// Activations [rows × k] bf16, row stride ld elements; box 64 k × box_rows,
-// 128-byte swizzle (the UMMA K-major SW128 layout), OOB -> zero.
+// Activations [rows × k] bf16, row stride ld elements, viewed as 3-D
+// {64 k, rows, k/64 slices}: one TMA box {64, box_rows, slices} lands
+// `slices` consecutive [box_rows × 64] sub-tiles, each in the UMMA K-major
+// 128-byte-swizzle layout. OOB (ragged k / rows) -> zero.
 hp_status make_act_map(CUtensorMap* map, const void* x, int64_t k, int64_t rows,
-                       int64_t ld, int box_rows) {
+                       int64_t ld, int box_rows, int slices) {
     encode_fn enc = get_encode();
     if (!enc) return fail(HP_ECUDA, "cuTensorMapEncodeTiled unavailable");
-    cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows)};
-    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
-    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x), dims,
+    // innermost dim covers exactly 64 elements per slice; k padded to 64
+    const int64_t nslices = (k + 63) / 64;
+    cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(nslices)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 2, 128};
+    cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(slices)};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(x), dims,
                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -150,6 +158,14 @@ int hp_abi_version(void) { return 1; }
 int hp_device_ok(void) { return device_ok_cached(); }
 
 void hp_set_sm_budget(int sms) { hp::g_sm_budget = sms > 0 ? sms : 0; }
+
+/* debug: copy the HP_QGEMM_TRACE clock trace (4 roles x 64 iters x 4 events) */
+int hp_debug_trace(unsigned long long* host, int n) {
+    if (!hp::g_trace) return 0;
+    cudaDeviceSynchronize();
+    cudaMemcpy(host, hp::g_trace, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost);
+    return n;
+}
 
 int64_t hp_packed_bytes(int64_t n_out, int64_t k_in, int bits) {
     if (n_out <= 0 || k_in <= 0 || !bits_ok(bits)) return -1;
@@ -250,7 +266,8 @@ hp_status hp_qlinear(const hp_qweight* w, const void* x, int64_t ldx, int64_t m,
         return fail(HP_EINVAL, "qlinear: workspace too small (need " +
                                    std::to_string(p.workspace) + " bytes)");
     CUtensorMap map;
-    if (hp_status s = make_act_map(&map, x, w->k_in, m, ldx, p.bn)) return s;
+    if (hp_status s = make_act_map(&map, x, w->k_in, m, ldx, p.bn, 2 * hp::groups_per_stage(p.bn)))
+        return s;
     return cuda_status(hp::launch_qgemm(map, p, w->bits, w->scheme == HP_SYMMETRIC, w->packed,
                                         w->scale, w->zero, w->n_out, w->k_in, m, y, ldy,
                                         residual, ldr, epilogue, workspace,

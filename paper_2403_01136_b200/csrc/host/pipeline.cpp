@@ -54,6 +54,17 @@ void hp_ok(hp_status s, const char* what) {
         throw std::runtime_error(std::string("pipeline: ") + what + ": " + hp_last_error());
 }
 
+// Timing events inside a captured round must stay real event records (an
+// internal graph event node cannot be timed): record them as "external".
+cudaError_t timing_record(cudaEvent_t e, cudaStream_t st) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaError_t r = cudaStreamIsCapturing(st, &cap);
+    if (r != cudaSuccess) return r;
+    if (cap == cudaStreamCaptureStatusActive)
+        return cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+    return cudaEventRecord(e, st);
+}
+
 uint64_t splitmix(uint64_t z) {
     z += 0x9E3779B97F4A7C15ull;
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -328,11 +339,11 @@ struct pipeline::impl {
 
     void qlin(const opw& w, const void* x, int64_t ldx, int64_t m, void* y, int64_t ldy,
               const void* res, int epi, int phase, cudaEvent_t* evs) {
-        if (evs) cuda_ok(cudaEventRecord(evs[0], cs), "ev");
+        if (evs) cuda_ok(timing_record(evs[0], cs), "ev");
         hp_ok(hp_qlinear(&w.w, x, ldx, m, y, ldy, res, res ? ldy : 0, epi, phase, ws, ws_bytes,
                          cs),
               "qlinear");
-        if (evs) cuda_ok(cudaEventRecord(evs[1], cs), "ev");
+        if (evs) cuda_ok(timing_record(evs[1], cs), "ev");
     }
 
     // forward of this stage's layers, in place on x [m x h1]
@@ -406,9 +417,9 @@ struct pipeline::impl {
             void* x = pre ? prefill_ptr(u.index) : dec_x[u.index];
             const int64_t m = pre ? prefill_rows(u.index) : group_size[u.index];
             const int phase = pre ? HP_PREFILL : HP_DECODE;
-            cuda_ok(cudaEventRecord(unit_ev[2 * ui], cs), "ev");
+            cuda_ok(timing_record(unit_ev[2 * ui], cs), "ev");
             forward(x, m, phase, opt.instrument && instr_unit[phase] == static_cast<int>(ui));
-            cuda_ok(cudaEventRecord(unit_ev[2 * ui + 1], cs), "ev");
+            cuda_ok(timing_record(unit_ev[2 * ui + 1], cs), "ev");
 
             // ---- output
             if (!last) {

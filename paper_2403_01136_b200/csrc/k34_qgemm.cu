@@ -20,12 +20,13 @@
 // Pipelines: smem stages full/empty (producer<->MMA), TMEM A stages
 // afull/aempty (dequant<->MMA), accumulator buffers tfull/tempty
 // (MMA<->epilogue).
-// Decode (K3, M = xi <= 32): BN = 16/32 and split-K so every SM streams
-// weights; HBM-bound. Prefill (K4, M = eta*s): BN = 128/256, no split;
+// Decode (K3, M = xi <= 32): BN = 16/32 and stream-K (each CTA streams an
+// equal contiguous range of weight groups; HBM-bound). Prefill (K4, M = eta*s): BN = 128/256, no split;
 // tensor-bound.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cstdint>
+#include <cstdlib>
 
 #include "layout.cuh"
 #include "sm100.cuh"
@@ -41,23 +42,100 @@ struct qgemm_args {
     const float* zero;
     int n_out, k_in, G, NT;
     int m, MT;
-    int splits, gps;  // k-splits, groups per split
-    int num_units;
+    int stream_k;       // 1: contiguous group ranges per CTA (decode), 0: whole tiles
+    int64_t total;      // MT*NT*G group-steps (stream-K)
+    int maxseg;         // partial slots per tile (stream-K)
     __nv_bfloat16* y;
     int64_t ldy;
     const __nv_bfloat16* res;
     int64_t ldr;
     int epi;
-    float* partial;     // [splits][MT*BN][n_out] fp32 (splits > 1)
-    unsigned* counters; // [MT*NT]
+    float* partial;     // [tiles][maxseg][128][BN] fp32
+    unsigned* counters; // [tiles]
+    unsigned long long* trace;  // optional per-role clock trace of CTA 0
 };
 
-template <int BITS, int BN>
+// Debug trace (HP_QGEMM_TRACE): CTA 0 records %globaltimer at pipeline
+// events: slot = role*kTraceIters*4 + iter*4 + event.
+constexpr int kTraceIters = 64;
+__device__ __forceinline__ void trace_ev(const qgemm_args& a, int role, uint32_t it, int ev) {
+    if (a.trace && blockIdx.x == 0 && it < kTraceIters) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.trace[(role * kTraceIters + it) * 4 + ev] = t;
+    }
+}
+
+// A work segment: groups [g0, g1) of output tile `tile` (= mt*NT + nt).
+// Stream-K: CTA c owns group-steps [c*total/P, (c+1)*total/P) of the
+// tile-major order; a tile split over several CTAs is reduced by the last
+// one to finish, summing the partials in segment order (deterministic).
+struct seg_t {
+    int tile, g0, g1, idx, nseg;
+};
+
+__device__ __forceinline__ int64_t sk_lo(int64_t c, int64_t total, int64_t P) {
+    return (c * total) / P;
+}
+// CTA owning group-step w
+__device__ __forceinline__ int sk_owner(int64_t w, int64_t total, int64_t P) {
+    int64_t c = (w * P) / total;
+    while (c + 1 < P && sk_lo(c + 1, total, P) <= w) ++c;
+    while (c > 0 && sk_lo(c, total, P) > w) --c;
+    return static_cast<int>(c);
+}
+
+// Stream-K segments are visited with the CTA's LAST segment first: the head
+// of the tile that the next CTA finishes early, so both halves of every
+// split tile complete (and get reduced) early instead of at the kernel tail.
+struct seg_iter {
+    // unit mode
+    int u;
+    // stream-K mode
+    int64_t w, w1, wlo, wlast;
+    int phase;  // 0: last segment, 1: the others in order
+    __device__ __forceinline__ void init(const qgemm_args& a) {
+        u = blockIdx.x;
+        wlo = sk_lo(blockIdx.x, a.total, gridDim.x);
+        w1 = sk_lo(blockIdx.x + 1, a.total, gridDim.x);
+        // start of the last segment = max(wlo, start of the tile holding w1-1)
+        const int64_t tstart = w1 > 0 ? ((w1 - 1) / a.G) * a.G : 0;
+        wlast = tstart > wlo ? tstart : wlo;
+        w = wlast;
+        phase = 0;
+    }
+    __device__ __forceinline__ bool next(const qgemm_args& a, seg_t& s) {
+        if (!a.stream_k) {
+            if (u >= a.MT * a.NT) return false;
+            s = {u, 0, a.G, 0, 1};
+            u += gridDim.x;
+            return true;
+        }
+        if (phase == 0 && w >= w1) {  // last segment done -> the rest
+            phase = 1;
+            w = wlo;
+        }
+        const int64_t lim = phase == 0 ? w1 : wlast;
+        if (w >= lim) return false;
+        const int tile = static_cast<int>(w / a.G);
+        const int g0 = static_cast<int>(w % a.G);
+        const int64_t tend = static_cast<int64_t>(tile + 1) * a.G;
+        const int64_t wend = lim < tend ? lim : tend;
+        const int first = sk_owner(static_cast<int64_t>(tile) * a.G, a.total, gridDim.x);
+        const int last = sk_owner(tend - 1, a.total, gridDim.x);
+        s = {tile, g0, g0 + static_cast<int>(wend - w), static_cast<int>(blockIdx.x) - first,
+             last - first + 1};
+        w = wend;
+        return true;
+    }
+};
+
+template <int BITS, int BN, int GPS>
 struct qgemm_cfg {
     static constexpr int kThreads = 512;
-    static constexpr int kB = BN * 256;                 // two 64-k swizzled sub-tiles
-    static constexpr int kCodes = BITS * 2048;
-    static constexpr int kScale = BITS == 16 ? 0 : 1024; // scale + zero rows
+    static constexpr int kB = BN * 256 * GPS;                 // 2*GPS 64-k swizzled slices
+    static constexpr int kCodes = BITS * 2048 * GPS;
+    static constexpr int kScale = BITS == 16 ? 0 : 1024 * GPS;  // GPS scale rows + GPS zero rows
     static constexpr int kStage = kB + kCodes + kScale;
     static constexpr int kBudget = 200 * 1024;
     static constexpr int SS_ = kBudget / kStage;
@@ -65,7 +143,8 @@ struct qgemm_cfg {
     static constexpr int NACC = BN <= 128 ? 2 : 1;
     static constexpr int A0_ = NACC * BN < 64 ? 64 : NACC * BN;
     static constexpr int A0 = (A0_ + 63) / 64 * 64;
-    static constexpr int AS_ = (512 - A0) / 64;
+    static constexpr int ACOLS = 64 * GPS;                    // TMEM columns per A stage
+    static constexpr int AS_ = (512 - A0) / ACOLS;
     static constexpr int AS = AS_ > 8 ? 8 : AS_;
     static constexpr int kBarOff = SS * kStage;
     static constexpr int kSmem = kBarOff + 256 + 1024;  // + barriers + align slack
@@ -73,10 +152,27 @@ struct qgemm_cfg {
     static_assert(AS >= 2, "need >= 2 TMEM A stages");
 };
 
-template <int BITS, bool SYM, int BN>
+// Epilogue store of `CNT` consecutive tokens of output column n (fully
+// unrolled, predicated: the values stay in registers).
+template <int CNT>
+__device__ __forceinline__ void store_out(const qgemm_args& a, int t0, int n, const float (&v)[CNT]) {
+    if (n >= a.n_out) return;
+#pragma unroll
+    for (int i = 0; i < CNT; ++i) {
+        const int t = t0 + i;
+        if (t < a.m) {
+            float f = v[i];
+            if (a.epi & 1) f = fmaxf(f, 0.0f);
+            if (a.res) f += __bfloat162float(a.res[t * a.ldr + n]);
+            a.y[t * a.ldy + n] = __float2bfloat16_rn(f);
+        }
+    }
+}
+
+template <int BITS, bool SYM, int BN, int GPS>
 __global__ void __launch_bounds__(512, 1)
     qgemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const qgemm_args a) {
-    using C = qgemm_cfg<BITS, BN>;
+    using C = qgemm_cfg<BITS, BN, GPS>;
     constexpr int SS = C::SS, AS = C::AS, NACC = C::NACC;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -86,6 +182,7 @@ __global__ void __launch_bounds__(512, 1)
     auto stage_scale = [&](int s) {
         return reinterpret_cast<float*>(smem + s * C::kStage + C::kB + C::kCodes);
     };
+    constexpr int kScaleRow = 128 * GPS;  // floats: scales of the stage's groups, then zeros
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
     uint64_t* full = bars;
     uint64_t* empty = full + SS;
@@ -96,8 +193,15 @@ __global__ void __launch_bounds__(512, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NACC);
     unsigned* bcast = tmem_slot + 1;
 
-    const int warp = threadIdx.x >> 5;
+    // warp index broadcast from lane 0: provably warp-uniform for the
+    // compiler, so role code runs on the uniform datapath (no R2UR)
+    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
     const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0 && a.trace) {  // per-CTA entry time
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.trace[4 * kTraceIters * 4 + 2 * blockIdx.x] = t;
+    }
 
     if (warp == 1 && lane == 0) {
         for (int i = 0; i < SS; ++i) {
@@ -119,105 +223,121 @@ __global__ void __launch_bounds__(512, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform
 
-    const int per_mt = a.NT * a.splits;
+    seg_iter iter;
+    iter.init(a);
+    seg_t sg;
 
     if (warp == 0) {
-        // ===================== producer =====================
-        if (lane == 0) {
-            constexpr uint32_t kBytes = C::kB + C::kCodes + (BITS == 16 ? 0 : (SYM ? 512 : 1024));
-            uint32_t it = 0;
-            for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
-                const int mt = u / per_mt, rem = u % per_mt;
-                const int nt = rem / a.splits, sp = rem % a.splits;
-                const int g0 = sp * a.gps;
-                const int g1 = min(a.G, g0 + a.gps);
-                for (int g = g0; g < g1; ++g, ++it) {
-                    const int s = it % SS;
-                    mbar_wait(&empty[s], ((it / SS) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&full[s], kBytes);
-                    const size_t t = static_cast<size_t>(nt) * a.G + g;
-                    bulk_g2s(stage_codes(s), a.packed + t * C::kCodes, C::kCodes, &full[s]);
-                    if constexpr (BITS != 16) {
-                        bulk_g2s(stage_scale(s), a.scale + t * 128, 512, &full[s]);
-                        if constexpr (!SYM)
-                            bulk_g2s(stage_scale(s) + 128, a.zero + t * 128, 512, &full[s]);
-                    }
-                    tma_load_2d(stage_b(s), &tmap_x, g * 128, mt * BN, &full[s]);
-                    tma_load_2d(stage_b(s) + BN * 128, &tmap_x, g * 128 + 64, mt * BN, &full[s]);
+        // ===================== producer (whole warp, elected issue) ============
+        uint32_t it = 0;
+        while (iter.next(a, sg)) {
+            const int mt = sg.tile / a.NT, nt = sg.tile % a.NT;
+            for (int g = sg.g0; g < sg.g1; g += GPS, ++it) {
+                const int ng = min(GPS, sg.g1 - g);
+                const int s = it % SS;
+                trace_ev(a, 0, it, 0);
+                mbar_wait_warp(&empty[s], ((it / SS) & 1) ^ 1);
+                trace_ev(a, 0, it, 1);
+                const uint32_t cbytes = static_cast<uint32_t>(ng) * BITS * 2048;
+                const uint32_t sbytes = BITS == 16 ? 0u : static_cast<uint32_t>(ng) * 512u * (SYM ? 1 : 2);
+                mbar_arrive_expect_tx_elect(&full[s], static_cast<uint32_t>(C::kB) + cbytes + sbytes);
+                const size_t t = static_cast<size_t>(nt) * a.G + g;
+                bulk_g2s_elect(stage_codes(s), a.packed + t * (BITS * 2048), cbytes, &full[s]);
+                if constexpr (BITS != 16) {
+                    bulk_g2s_elect(stage_scale(s), a.scale + t * 128, ng * 512u, &full[s]);
+                    if constexpr (!SYM)
+                        bulk_g2s_elect(stage_scale(s) + kScaleRow, a.zero + t * 128, ng * 512u, &full[s]);
                 }
+                tma_load_3d_elect(stage_b(s), &tmap_x, 0, mt * BN, g * 2, &full[s]);
+                trace_ev(a, 0, it, 2);
             }
         }
     } else if (warp == 1) {
-        // ===================== MMA issuer =====================
-        if (lane == 0) {
-            constexpr uint32_t idesc = umma_idesc_bf16(128, BN);
-            uint32_t it = 0, ut = 0;
-            for (int u = blockIdx.x; u < a.num_units; u += gridDim.x, ++ut) {
-                const int rem = u % per_mt;
-                const int sp = rem % a.splits;
-                const int g0 = sp * a.gps;
-                const int g1 = min(a.G, g0 + a.gps);
-                const int acc = ut % NACC;
-                mbar_wait(&tempty[acc], ((ut / NACC) & 1) ^ 1);
+        // ===================== MMA issuer (whole warp, elected issue) ==========
+        constexpr uint32_t idesc = umma_idesc_bf16(128, BN);
+        uint32_t it = 0, ut = 0;
+        while (iter.next(a, sg)) {
+            const int acc = ut % NACC;
+            mbar_wait_warp(&tempty[acc], ((ut / NACC) & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t d_tmem = tmem + acc * BN;
+            for (int g = sg.g0; g < sg.g1; g += GPS, ++it) {
+                const int ng = min(GPS, sg.g1 - g);
+                const int s = it % SS, as = it % AS;
+                trace_ev(a, 1, it, 0);
+                mbar_wait_warp(&full[s], (it / SS) & 1);
+                trace_ev(a, 1, it, 1);
+                mbar_wait_warp(&afull[as], (it / AS) & 1);
+                trace_ev(a, 1, it, 2);
                 tc_fence_after();
-                const uint32_t d_tmem = tmem + acc * BN;
-                for (int g = g0; g < g1; ++g, ++it) {
-                    const int s = it % SS, as = it % AS;
-                    mbar_wait(&full[s], (it / SS) & 1);
-                    mbar_wait(&afull[as], (it / AS) & 1);
-                    tc_fence_after();
-                    const uint32_t bbase = smem_u32(stage_b(s));
+                const uint32_t bbase = smem_u32(stage_b(s));
+                const uint32_t abase = tmem + C::A0 + as * C::ACOLS;
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
+                for (int j = 0; j < 8 * GPS; ++j) {
+                    if (j < 8 * ng) {
                         const uint64_t bdesc =
                             umma_desc_sw128(bbase + (j >> 2) * (BN * 128) + (j & 3) * 32);
-                        mma_ts(d_tmem, tmem + C::A0 + as * 64 + j * 8, bdesc, idesc,
-                               (g > g0 || j > 0) ? 1u : 0u);
+                        mma_ts_elect(d_tmem, abase + j * 8, bdesc, idesc,
+                                     (g > sg.g0 || j > 0) ? 1u : 0u);
                     }
-                    tc_commit(&empty[s]);
-                    tc_commit(&aempty[as]);
                 }
-                tc_commit(&tfull[acc]);
+                tc_commit_elect(&empty[s]);
+                tc_commit_elect(&aempty[as]);
+                trace_ev(a, 1, it, 3);
             }
+            tc_commit_elect(&tfull[acc]);
+            ++ut;
         }
     } else if (warp >= 4 && warp < 12) {
         // ===================== dequant =====================
         const int q = warp - 4;
         const int lq = warp & 3;  // TMEM lane quarter of this warp
-        const int kh = q >> 2;    // which 64-k half of each group
+        const int kh = q >> 2;    // warpgroup: slices [kh*2*GPS, (kh+1)*2*GPS) of a stage
         const int r = lq * 32 + lane;
         const uint32_t lane_addr = static_cast<uint32_t>(lq * 32) << 16;
         uint32_t it = 0;
-        for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
-            const int rem = u % per_mt;
-            const int sp = rem % a.splits;
-            const int g0 = sp * a.gps;
-            const int g1 = min(a.G, g0 + a.gps);
-            for (int g = g0; g < g1; ++g, ++it) {
+        while (iter.next(a, sg)) {
+            for (int g = sg.g0; g < sg.g1; g += GPS, ++it) {
+                const int ng = min(GPS, sg.g1 - g);
                 const int s = it % SS, as = it % AS;
+                const int trole = (lane == 0 && warp == 4) ? 2 : -1;
+                if (trole >= 0) trace_ev(a, trole, it, 0);
                 mbar_wait(&full[s], (it / SS) & 1);
+                if (trole >= 0) trace_ev(a, trole, it, 1);
                 mbar_wait(&aempty[as], ((it / AS) & 1) ^ 1);
+                if (trole >= 0) trace_ev(a, trole, it, 2);
                 tc_fence_after();
-                float sf = 0.f, zf = 0.f;
-                if constexpr (BITS != 16) {
-                    sf = stage_scale(s)[r];
-                    if constexpr (!SYM) zf = stage_scale(s)[128 + r];
-                }
-                const uint32_t s2 = bf16x2_splat_bits(sf), z2 = bf16x2_splat_bits(zf);
-                const uint8_t* rowc = stage_codes(s) + r * 16;
+                // This warpgroup's share of the stage: GPS == 2 -> group kh (4 slices);
+                // GPS == 1 -> slices 2kh, 2kh+1 of group 0.
+                constexpr int kSl = GPS == 2 ? 4 : 2;
+                const int gi = GPS == 2 ? kh : 0;
+                const int sl0 = GPS == 2 ? 0 : 2 * kh;
+                if (gi < ng) {
+                    const uint32_t sbase = smem_u32(stage_codes(s)) + gi * (BITS * 2048) + r * 16;
+                    slice_words<BITS> wv[kSl];
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int sl = kh * 2 + h;
-                    uint32_t v[16];
-                    dequant_slice32<BITS, SYM>(rowc, sl, sf, zf, s2, z2, v);
-                    tmem_st16(tmem + lane_addr + C::A0 + as * 64 + sl * 16, v);
+                    for (int h = 0; h < kSl; ++h) load_slice<BITS>(sbase, sl0 + h, wv[h]);
+                    float sf = 0.f, zf = 0.f;
+                    if constexpr (BITS != 16) {
+                        const uint32_t saddr = smem_u32(stage_scale(s)) + (gi * 128 + r) * 4;
+                        sf = ldsf(saddr);
+                        if constexpr (!SYM) zf = ldsf(saddr + kScaleRow * 4);
+                    }
+                    const uint32_t s2 = bf16x2_splat_bits(sf), z2 = bf16x2_splat_bits(zf);
+#pragma unroll
+                    for (int h = 0; h < kSl; ++h) {
+                        uint32_t v[16];
+                        convert_slice<BITS, SYM>(wv[h], sf, zf, s2, z2, v);
+                        tmem_st16(tmem + lane_addr + C::A0 + as * C::ACOLS + gi * 64 + (sl0 + h) * 16, v);
+                    }
                 }
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&afull[as]);
+                if (trole >= 0) trace_ev(a, trole, it, 3);
             }
         }
     } else if (warp >= 12) {
@@ -226,74 +346,82 @@ __global__ void __launch_bounds__(512, 1)
         const int r = lq * 32 + lane;
         const uint32_t lane_addr = static_cast<uint32_t>(lq * 32) << 16;
         uint32_t ut = 0;
-        for (int u = blockIdx.x; u < a.num_units; u += gridDim.x, ++ut) {
-            const int mt = u / per_mt, rem = u % per_mt;
-            const int nt = rem / a.splits, sp = rem % a.splits;
+        while (iter.next(a, sg)) {
+            const int mt = sg.tile / a.NT, nt = sg.tile % a.NT;
             const int acc = ut % NACC;
             const int n = nt * 128 + r;
+            if (threadIdx.x == 384) trace_ev(a, 3, 48 + ut, 0);
             mbar_wait(&tfull[acc], (ut / NACC) & 1);
+            if (threadIdx.x == 384) trace_ev(a, 3, 48 + ut, 1);
             tc_fence_after();
+            constexpr bool kSK = BN <= 64;  // stream-K only runs the decode tiles
+            float* part = (kSK && sg.nseg > 1) ? a.partial + ((static_cast<size_t>(sg.tile) * a.maxseg + sg.idx) * 128 + r) * BN
+                                      : nullptr;
+#pragma unroll 1
             for (int c0 = 0; c0 < BN; c0 += 16) {
                 uint32_t v[16];
                 tmem_ld16(tmem + lane_addr + acc * BN + c0, v);
                 tmem_ld_wait();
-                if (a.splits == 1) {
-                    if (n < a.n_out) {
+                if (kSK && part) {
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) {
-                            const int t = mt * BN + c0 + i;
-                            if (t < a.m) {
-                                float f = __uint_as_float(v[i]);
-                                if (a.epi & 1) f = fmaxf(f, 0.0f);
-                                if (a.res) f += __bfloat162float(a.res[t * a.ldr + n]);
-                                a.y[t * a.ldy + n] = __float2bfloat16_rn(f);
-                            }
-                        }
-                    }
+                    for (int i = 0; i < 16; i += 4)
+                        __stcg(reinterpret_cast<float4*>(part + c0 + i),
+                               make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
+                                           __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3])));
                 } else {
-                    float* dst = a.partial + (static_cast<size_t>(sp) * a.MT * BN +
-                                              static_cast<size_t>(mt) * BN + c0) * a.n_out;
-                    if (n < a.n_out) {
+                    float f[16];
 #pragma unroll
-                        for (int i = 0; i < 16; ++i)
-                            dst[static_cast<size_t>(i) * a.n_out + n] = __uint_as_float(v[i]);
-                    }
+                    for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]);
+                    store_out<16>(a, mt * BN + c0, n, f);
                 }
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (threadIdx.x == 384) trace_ev(a, 3, 48 + ut, 2);
 
-            if (a.splits > 1) {
+            if constexpr (kSK) if (sg.nseg > 1) {
                 __threadfence();
                 asm volatile("bar.sync 1, 128;" ::: "memory");
                 if (warp == 12 && lane == 0)
-                    *bcast = atomicAdd(&a.counters[mt * a.NT + nt], 1u);
+                    *bcast = atomicAdd(&a.counters[sg.tile], 1u);
                 asm volatile("bar.sync 1, 128;" ::: "memory");
-                if (*bcast == static_cast<unsigned>(a.splits - 1)) {
+                if (*bcast == static_cast<unsigned>(sg.nseg - 1)) {
                     __threadfence();
-                    if (n < a.n_out) {
-                        for (int i = 0; i < BN; ++i) {
-                            const int t = mt * BN + i;
-                            if (t >= a.m) break;
-                            float f = 0.f;
-                            for (int k = 0; k < a.splits; ++k)
-                                f += __ldcg(a.partial + (static_cast<size_t>(k) * a.MT * BN +
-                                                         static_cast<size_t>(mt) * BN + i) *
-                                                            a.n_out + n);
-                            if (a.epi & 1) f = fmaxf(f, 0.0f);
-                            if (a.res) f += __bfloat162float(a.res[t * a.ldr + n]);
-                            a.y[t * a.ldy + n] = __float2bfloat16_rn(f);
+                    // ordered reduction of all segments of this tile (row r)
+                    const float* base = a.partial + (static_cast<size_t>(sg.tile) * a.maxseg * 128 + r) * BN;
+                    float accv[BN];
+#pragma unroll
+                    for (int i = 0; i < BN; ++i) accv[i] = 0.f;
+                    for (int j = 0; j < sg.nseg; ++j) {
+                        const float4* src = reinterpret_cast<const float4*>(base + static_cast<size_t>(j) * 128 * BN);
+                        float4 tmp[BN / 4];
+#pragma unroll
+                        for (int i = 0; i < BN / 4; ++i) tmp[i] = __ldcg(src + i);
+#pragma unroll
+                        for (int i = 0; i < BN / 4; ++i) {
+                            accv[4 * i] += tmp[i].x;
+                            accv[4 * i + 1] += tmp[i].y;
+                            accv[4 * i + 2] += tmp[i].z;
+                            accv[4 * i + 3] += tmp[i].w;
                         }
                     }
-                    if (warp == 12 && lane == 0) a.counters[mt * a.NT + nt] = 0u;
+                    store_out<BN>(a, mt * BN, n, accv);
+                    if (warp == 12 && lane == 0) a.counters[sg.tile] = 0u;
                 }
                 asm volatile("bar.sync 1, 128;" ::: "memory");
             }
+            if (threadIdx.x == 384) trace_ev(a, 3, 48 + ut, 3);
+            ++ut;
         }
     }
 
     __syncthreads();
+    if (threadIdx.x == 0 && a.trace) {  // per-CTA exit time
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.trace[4 * kTraceIters * 4 + 2 * blockIdx.x + 1] = t;
+    }
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc<512>(tmem);
@@ -303,6 +431,13 @@ __global__ void __launch_bounds__(512, 1)
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
+// groups of 128 k per pipeline stage: decode tiles move 2 groups per stage to
+// amortise the per-stage barrier/issue work; prefill stages are MMA-heavy.
+template <int BN>
+constexpr int kGroupsPerStage = BN <= 64 ? 2 : 1;
+
+int groups_per_stage(int bn) { return bn <= 64 ? 2 : 1; }
+
 namespace {
 
 int g_num_sms = 0;
@@ -321,16 +456,17 @@ int num_sms() {
 template <int BITS, bool SYM, int BN>
 cudaError_t launch_one(const CUtensorMap& map, const qgemm_args& a, int grid,
                        cudaStream_t st) {
-    using C = qgemm_cfg<BITS, BN>;
+    constexpr int GPS = kGroupsPerStage<BN>;
+    using C = qgemm_cfg<BITS, BN, GPS>;
     static bool attr_done = false;
     if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(qgemm_kernel<BITS, SYM, BN>,
+        cudaError_t e = cudaFuncSetAttribute(qgemm_kernel<BITS, SYM, BN, GPS>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              C::kSmem);
         if (e != cudaSuccess) return e;
         attr_done = true;
     }
-    qgemm_kernel<BITS, SYM, BN><<<grid, C::kThreads, C::kSmem, st>>>(map, a);
+    qgemm_kernel<BITS, SYM, BN, GPS><<<grid, C::kThreads, C::kSmem, st>>>(map, a);
     return cudaGetLastError();
 }
 
@@ -351,6 +487,8 @@ cudaError_t dispatch_bits(int bits, bool sym, const CUtensorMap& map,
 struct qgemm_plan {
     int bn, mt, splits, gps, units, grid;
     size_t workspace;
+    int stream_k, maxseg;
+    int64_t total;
 };
 
 qgemm_plan plan_qgemm(int64_t n_out, int64_t k_in, int64_t m, int phase) {
@@ -364,29 +502,40 @@ qgemm_plan plan_qgemm(int64_t n_out, int64_t k_in, int64_t m, int phase) {
         p.bn = m <= 128 ? 128 : 256;
     }
     p.mt = static_cast<int>(ceil_div64(m, p.bn));
+    const int64_t tiles = static_cast<int64_t>(p.mt) * NT;
     p.splits = 1;
-    if (phase == 1 && p.mt == 1) {
-        // minimise waves * groups-per-unit; prefer fewer splits on ties
-        long best = -1;
-        for (int s = 1; s <= 16 && s <= G; ++s) {
-            const long units = static_cast<long>(NT) * s;
-            const long cost = ((units + sms - 1) / sms) * ((G + s - 1) / s);
-            if (best < 0 || cost < best) {
-                best = cost;
-                p.splits = s;
-            }
+    p.gps = G;
+    p.units = static_cast<int>(tiles);
+    p.workspace = 0;
+    p.maxseg = 1;
+    p.total = tiles * G;
+    // stream-K when whole tiles would leave SMs idle or unbalanced
+    p.stream_k = (phase == 1 && tiles % sms != 0) ? 1 : 0;
+    if (p.stream_k) {
+        p.grid = static_cast<int>(p.total < sms ? p.total : sms);
+        const int64_t per = p.total / p.grid;  // >= 1 group-step per CTA
+        p.maxseg = static_cast<int>((G + per - 1) / per) + 1;
+        if (p.maxseg > p.grid) p.maxseg = p.grid;
+        p.workspace = 256 + (static_cast<size_t>(tiles) * sizeof(unsigned) + 255) / 256 * 256 +
+                      static_cast<size_t>(tiles) * p.maxseg * 128 * p.bn * sizeof(float);
+    } else {
+        p.grid = static_cast<int>(tiles < sms ? tiles : sms);
+    }
+    return p;
+}
+
+unsigned long long* g_trace = nullptr;
+
+unsigned long long* trace_buffer() {
+    static bool checked = false;
+    if (!checked) {
+        checked = true;
+        if (getenv("HP_QGEMM_TRACE")) {
+            cudaMalloc(&g_trace, sizeof(unsigned long long) * (4 * kTraceIters * 4 + 2 * 1024));
+            cudaMemset(g_trace, 0, sizeof(unsigned long long) * (4 * kTraceIters * 4 + 2 * 1024));
         }
     }
-    p.gps = (G + p.splits - 1) / p.splits;
-    p.splits = (G + p.gps - 1) / p.gps;  // no empty splits
-    p.units = p.mt * NT * p.splits;
-    p.grid = p.units < sms ? p.units : sms;
-    p.workspace = 0;
-    if (p.splits > 1)
-        p.workspace = 256 +
-                      (static_cast<size_t>(p.mt) * NT * sizeof(unsigned) + 255) / 256 * 256 +
-                      static_cast<size_t>(p.splits) * p.mt * p.bn * n_out * sizeof(float);
-    return p;
+    return g_trace;
 }
 
 cudaError_t launch_qgemm(const CUtensorMap& map, const qgemm_plan& p, int bits,
@@ -405,15 +554,16 @@ cudaError_t launch_qgemm(const CUtensorMap& map, const qgemm_plan& p, int bits,
     a.NT = static_cast<int>(ceil_div64(n_out, 128));
     a.m = static_cast<int>(m);
     a.MT = p.mt;
-    a.splits = p.splits;
-    a.gps = p.gps;
-    a.num_units = p.units;
+    a.stream_k = p.stream_k;
+    a.total = p.total;
+    a.maxseg = p.maxseg;
     a.y = static_cast<__nv_bfloat16*>(y);
     a.ldy = ldy;
     a.res = static_cast<const __nv_bfloat16*>(res);
     a.ldr = ldr;
     a.epi = epi;
-    if (p.splits > 1) {
+    a.trace = trace_buffer();
+    if (p.stream_k) {
         auto* base = static_cast<uint8_t*>(workspace);
         a.counters = reinterpret_cast<unsigned*>(base);
         a.partial = reinterpret_cast<float*>(

@@ -103,6 +103,9 @@ __device__ __forceinline__ uint32_t bf16x2_splat_bits(float f) {
 template <bool SYM>
 __device__ __forceinline__ uint32_t finish_pair(uint32_t v, uint32_t negoff2,
                                                 uint32_t s2, uint32_t z2) {
+#ifdef HP_EXPERIMENT_RAW
+    return v;  // timing experiment only: raw magic codes, no scale
+#endif
     constexpr uint32_t one2 = 0x3F803F80u;  // bf16 1.0 x2
     uint32_t c;
     asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(c) : "r"(v), "r"(one2), "r"(negoff2));
@@ -113,6 +116,79 @@ __device__ __forceinline__ uint32_t finish_pair(uint32_t v, uint32_t negoff2,
         asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(c), "r"(s2), "r"(z2));
     }
     return d;
+}
+
+// Raw code words of one 32-element slice (loaded ahead of the conversion so
+// the shared-memory latency of all slices overlaps).
+template <int BITS>
+struct slice_words {
+    static constexpr int N = BITS == 3 ? 3 : (BITS == 4 ? 4 : (BITS == 8 ? 8 : 16));
+    uint32_t w[N];
+};
+
+// row_chunks: SHARED-space byte address of the row's first 16-byte piece
+template <int BITS>
+__device__ __forceinline__ void load_slice(uint32_t row_chunks, int slice,
+                                           slice_words<BITS>& o) {
+    if constexpr (BITS == 4) {
+        const uint4 q = lds128(row_chunks + slice * 2048);
+        o.w[0] = q.x; o.w[1] = q.y; o.w[2] = q.z; o.w[3] = q.w;
+    } else if constexpr (BITS == 3) {
+        const uint2 lo = lds64(row_chunks + (slice >> 1) * 2048 + 8 * (slice & 1));
+        o.w[0] = lo.x; o.w[1] = lo.y;
+        o.w[2] = lds32(row_chunks + 2 * 2048 + 4 * slice);
+    } else if constexpr (BITS == 8) {
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+            const uint4 q = lds128(row_chunks + (2 * slice + cc) * 2048);
+            o.w[4 * cc] = q.x; o.w[4 * cc + 1] = q.y; o.w[4 * cc + 2] = q.z; o.w[4 * cc + 3] = q.w;
+        }
+    } else {
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+            const uint4 q = lds128(row_chunks + (4 * slice + cc) * 2048);
+            o.w[4 * cc] = q.x; o.w[4 * cc + 1] = q.y; o.w[4 * cc + 2] = q.z; o.w[4 * cc + 3] = q.w;
+        }
+    }
+}
+
+template <int BITS, bool SYM>
+__device__ __forceinline__ void convert_slice(const slice_words<BITS>& in, float s, float z,
+                                              uint32_t s2, uint32_t z2, uint32_t* out) {
+    if constexpr (BITS == 4) {
+        constexpr uint32_t negoff2 = SYM ? 0xC307C307u : 0xC300C300u;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int p = 0; p < 4; ++p)
+                out[4 * j + p] = finish_pair<SYM>(
+                    lop3_and_or(in.w[j] >> (4 * p), 0x000F000Fu, kMagic128), negoff2, s2, z2);
+    } else if constexpr (BITS == 3) {
+        constexpr uint32_t negoff2 = SYM ? 0xC303C303u : 0xC300C300u;
+        const uint32_t hb = in.w[2];
+#pragma unroll
+        for (int p = 0; p < 16; ++p) {
+            const uint32_t lw = p < 8 ? in.w[0] : in.w[1];
+            const uint32_t a = lop3_and_or(lw >> (2 * (p & 7)), 0x00030003u, kMagic128);
+            const uint32_t h = (p >= 2) ? (hb >> (p - 2)) : (hb << (2 - p));
+            out[p] = finish_pair<SYM>(lop3_and_or(h, 0x00040004u, a), negoff2, s2, z2);
+        }
+    } else if constexpr (BITS == 8) {
+        const float off = SYM ? 8388608.0f + 127.0f : 8388608.0f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                const float f0 = __uint_as_float(prmt(in.w[j], 0x4B000000u, 0x7540u + 2 * p)) - off;
+                const float f1 = __uint_as_float(prmt(in.w[j], 0x4B000000u, 0x7541u + 2 * p)) - off;
+                const float d0 = SYM ? f0 * s : __fmaf_rn(f0, s, z);
+                const float d1 = SYM ? f1 * s : __fmaf_rn(f1, s, z);
+                out[2 * j + p] = pack_bf16x2(d0, d1);
+            }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) out[i] = in.w[i];
+    }
 }
 
 // s, z: the row's fp32 scale / zero; s2, z2: their bf16x2 splats.

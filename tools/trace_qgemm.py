@@ -1,0 +1,49 @@
+"""Per-role pipeline trace of CTA 0 of one decode qlinear (HP_QGEMM_TRACE)."""
+import ctypes as C
+import os
+import sys
+from pathlib import Path
+
+os.environ["HP_QGEMM_TRACE"] = "1"
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+
+def main():
+    import numpy as np
+    import torch
+    from paper_2403_01136_b200 import qweight
+    from paper_2403_01136_b200.capi import lib
+    lib.hp_debug_trace.argtypes = [C.c_void_p, C.c_int]
+    n, k, bits, m = (int(v) for v in (sys.argv[1:] + ["20480", "5120", "4", "32"])[:4])
+    dev = torch.device("cuda:0")
+    w = (torch.randn(n, k, device=dev) * 0.02).to(torch.bfloat16)
+    qw = qweight.quantize(w, bits)
+    x = torch.randn(m, k, device=dev).to(torch.bfloat16)
+    for _ in range(3):
+        qweight.qlinear(qw, x, phase=1)
+    torch.cuda.synchronize()
+    buf = np.zeros(4 * 64 * 4 + 2 * 1024, dtype=np.uint64)
+    lib.hp_debug_trace(buf.ctypes.data, buf.size)
+    cta = buf[4 * 64 * 4:].reshape(1024, 2).astype(np.int64)
+    cta = cta[cta[:, 0] > 0]
+    t0c = cta[:, 0].min()
+    ent = (cta[:, 0] - t0c) / 1000
+    ext = (cta[:, 1] - t0c) / 1000
+    print(f"CTAs {len(cta)}: entry min/med/max {ent.min():.2f}/{np.median(ent):.2f}/{ent.max():.2f} us; "
+          f"exit min/med/max {ext.min():.2f}/{np.median(ext):.2f}/{ext.max():.2f} us")
+    print("  exit sorted (last 10):", np.round(np.sort(ext)[-10:], 2), " argmax", int(np.argmax(ext)))
+    t = buf[:4 * 64 * 4].reshape(4, 64, 4).astype(np.int64)
+    t0 = t[t > 0].min()
+    names = ["producer (start, empty_ok, issued)", "mma (start, full_ok, afull_ok, committed)",
+             "dequant w4 (start, full_ok, aempty_ok, arrived)", "epilogue seg (start, tfull_ok, stored, fixup_done) @48.., kernel entry/exit @63"]
+    for r in range(4):
+        print(names[r])
+        for it in range(0, 64):
+            row = t[r, it]
+            if row.max() == 0:
+                continue
+            print(f"  it={it:2d} " + " ".join(f"{(v - t0) / 1000:8.2f}" if v else "       -" for v in row))
+
+
+if __name__ == "__main__":
+    main()
