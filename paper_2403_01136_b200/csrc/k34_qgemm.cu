@@ -58,8 +58,9 @@ struct qgemm_args {
 // Debug trace (HP_QGEMM_TRACE): CTA 0 records %globaltimer at pipeline
 // events: slot = role*kTraceIters*4 + iter*4 + event.
 constexpr int kTraceIters = 64;
+__device__ int g_trace_cta = 0;
 __device__ __forceinline__ void trace_ev(const qgemm_args& a, int role, uint32_t it, int ev) {
-    if (a.trace && blockIdx.x == 0 && it < kTraceIters) {
+    if (a.trace && blockIdx.x == g_trace_cta && it < kTraceIters) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         a.trace[(role * kTraceIters + it) * 4 + ev] = t;
@@ -197,10 +198,12 @@ __global__ void __launch_bounds__(512, 1)
     // compiler, so role code runs on the uniform datapath (no R2UR)
     const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
     const int lane = threadIdx.x & 31;
+    long long clk0 = 0;
     if (threadIdx.x == 0 && a.trace) {  // per-CTA entry time
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         a.trace[4 * kTraceIters * 4 + 2 * blockIdx.x] = t;
+        clk0 = clock64();
     }
 
     if (warp == 1 && lane == 0) {
@@ -421,6 +424,7 @@ __global__ void __launch_bounds__(512, 1)
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         a.trace[4 * kTraceIters * 4 + 2 * blockIdx.x + 1] = t;
+        a.trace[4 * kTraceIters * 4 + 2048 + blockIdx.x] = static_cast<unsigned long long>(clock64() - clk0);
     }
     if (warp == 2) {
         tc_fence_after();
@@ -531,8 +535,10 @@ unsigned long long* trace_buffer() {
     if (!checked) {
         checked = true;
         if (getenv("HP_QGEMM_TRACE")) {
-            cudaMalloc(&g_trace, sizeof(unsigned long long) * (4 * kTraceIters * 4 + 2 * 1024));
-            cudaMemset(g_trace, 0, sizeof(unsigned long long) * (4 * kTraceIters * 4 + 2 * 1024));
+            int cta = getenv("HP_QGEMM_TRACE_CTA") ? atoi(getenv("HP_QGEMM_TRACE_CTA")) : 0;
+            cudaMemcpyToSymbol(g_trace_cta, &cta, sizeof(int));
+            cudaMalloc(&g_trace, sizeof(unsigned long long) * (4 * kTraceIters * 4 + 3 * 1024));
+            cudaMemset(g_trace, 0, sizeof(unsigned long long) * (4 * kTraceIters * 4 + 3 * 1024));
         }
     }
     return g_trace;

@@ -22,9 +22,10 @@ def main():
     for _ in range(3):
         qweight.qlinear(qw, x, phase=1)
     torch.cuda.synchronize()
-    buf = np.zeros(4 * 64 * 4 + 2 * 1024, dtype=np.uint64)
+    buf = np.zeros(4 * 64 * 4 + 3 * 1024, dtype=np.uint64)
     lib.hp_debug_trace(buf.ctypes.data, buf.size)
-    cta = buf[4 * 64 * 4:].reshape(1024, 2).astype(np.int64)
+    cyc = buf[4 * 64 * 4 + 2048:4 * 64 * 4 + 2048 + 148].astype(np.int64)
+    cta = buf[4 * 64 * 4:4 * 64 * 4 + 2048].reshape(1024, 2).astype(np.int64)
     cta = cta[cta[:, 0] > 0]
     t0c = cta[:, 0].min()
     ent = (cta[:, 0] - t0c) / 1000
@@ -32,6 +33,20 @@ def main():
     print(f"CTAs {len(cta)}: entry min/med/max {ent.min():.2f}/{np.median(ent):.2f}/{ent.max():.2f} us; "
           f"exit min/med/max {ext.min():.2f}/{np.median(ext):.2f}/{ext.max():.2f} us")
     print("  exit sorted (last 10):", np.round(np.sort(ext)[-10:], 2), " argmax", int(np.argmax(ext)))
+    span_ns = (cta[:148, 1] - cta[:148, 0]).astype(np.float64)
+    print(f"  CTA cycles/ns (implied GHz): median {np.median(cyc / span_ns):.3f}, cycles median {np.median(cyc):.0f}")
+    g = torch.cuda.CUDAGraph()
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        qweight.qlinear(qw, x, phase=1)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=st):
+            for _ in range(10):
+                qweight.qlinear(qw, x, phase=1)
+    g.replay(); torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(); g.replay(); e1.record(); torch.cuda.synchronize()
+    print(f"  graph b2b per launch: {e0.elapsed_time(e1) * 100:.1f} us")
     t = buf[:4 * 64 * 4].reshape(4, 64, 4).astype(np.int64)
     t0 = t[t > 0].min()
     names = ["producer (start, empty_ok, issued)", "mma (start, full_ok, afull_ok, committed)",
