@@ -60,7 +60,10 @@ struct qgemm_args {
 constexpr int kTraceIters = 64;
 __device__ int g_trace_cta = 0;
 __device__ __forceinline__ void trace_ev(const qgemm_args& a, int role, uint32_t it, int ev) {
-    if (a.trace && blockIdx.x == g_trace_cta && it < kTraceIters) {
+#ifndef HP_QGEMM_TRACE
+    return;  // production build: tracing compiled out
+#endif
+    if (role < 4 && a.trace && blockIdx.x == g_trace_cta && it < kTraceIters) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         a.trace[(role * kTraceIters + it) * 4 + ev] = t;
@@ -131,49 +134,106 @@ struct seg_iter {
     }
 };
 
-template <int BITS, int BN, int GPS>
+// A pipeline stage covers SPS 32-k "slices" (SPS = 8: two 128-k groups,
+// decode; SPS = 2: half a group, prefill — keeps the [BN x K] activation
+// tile per stage small so the pipeline is deep).
+template <int BITS, int BN, int SPS>
 struct qgemm_cfg {
     static constexpr int kThreads = 512;
-    static constexpr int kB = BN * 256 * GPS;                 // 2*GPS 64-k swizzled slices
-    static constexpr int kCodes = BITS * 2048 * GPS;
-    static constexpr int kScale = BITS == 16 ? 0 : 1024 * GPS;  // GPS scale rows + GPS zero rows
+    static constexpr int NG = SPS >= 4 ? SPS / 4 : 1;            // groups touched per stage
+    static constexpr int kB = BN * 64 * SPS;                     // SPS/2 64-k swizzled sub-tiles
+    static constexpr int kCodes = SPS >= 4 ? BITS * 2048 * NG
+                                           : (BITS == 3 ? 4096 : BITS * 1024);  // half group
+    static constexpr int kScale = BITS == 16 ? 0 : 1024 * NG;    // NG scale rows + NG zero rows
     static constexpr int kStage = kB + kCodes + kScale;
-    static constexpr int kBudget = 200 * 1024;
+    static constexpr int kBudget = 190 * 1024;
     static constexpr int SS_ = kBudget / kStage;
     static constexpr int SS = SS_ > 12 ? 12 : SS_;
     static constexpr int NACC = BN <= 128 ? 2 : 1;
     static constexpr int A0_ = NACC * BN < 64 ? 64 : NACC * BN;
     static constexpr int A0 = (A0_ + 63) / 64 * 64;
-    static constexpr int ACOLS = 64 * GPS;                    // TMEM columns per A stage
+    static constexpr int ACOLS = 16 * SPS;                       // TMEM columns per A stage
     static constexpr int AS_ = (512 - A0) / ACOLS;
     static constexpr int AS = AS_ > 8 ? 8 : AS_;
-    static constexpr int kBarOff = SS * kStage;
+    static constexpr int kStgOff = SS * kStage;               // epilogue staging [16][kStgLd] fp32
+    static constexpr int kStgLd = 132;
+    static constexpr int kBarOff = kStgOff + 16 * kStgLd * 4;
     static constexpr int kSmem = kBarOff + 256 + 1024;  // + barriers + align slack
     static_assert(SS >= 2, "need >= 2 smem stages");
     static_assert(AS >= 2, "need >= 2 TMEM A stages");
+    static_assert(SPS == 2 || SPS == 4 || SPS == 8, "SPS");
 };
 
-// Epilogue store of `CNT` consecutive tokens of output column n (fully
-// unrolled, predicated: the values stay in registers).
-template <int CNT>
-__device__ __forceinline__ void store_out(const qgemm_args& a, int t0, int n, const float (&v)[CNT]) {
-    if (n >= a.n_out) return;
+// Epilogue write-out of 16 tokens x 128 rows through shared memory: each
+// epilogue thread (row r) deposits its 16 fp32 accumulators transposed into
+// stg[t][r]; after a named barrier the 128 threads write the tile as 16-byte
+// vectors along n (coalesced), adding the residual in fp32 and rounding once
+// — the same arithmetic as a per-element epilogue, so results are identical.
+__device__ __forceinline__ void stage_store16(const qgemm_args& a, float* stg, int ldst, int r,
+                                              const float (&v)[16], int t0, int n0) {
 #pragma unroll
-    for (int i = 0; i < CNT; ++i) {
-        const int t = t0 + i;
-        if (t < a.m) {
-            float f = v[i];
-            if (a.epi & 1) f = fmaxf(f, 0.0f);
-            if (a.res) f += __bfloat162float(a.res[t * a.ldr + n]);
-            a.y[t * a.ldy + n] = __float2bfloat16_rn(f);
+    for (int i = 0; i < 16; ++i) stg[i * ldst + r] = v[i];
+    asm volatile("bar.sync 2, 128;" ::: "memory");
+    const int tid = threadIdx.x & 127;
+    const int t = tid >> 3;
+    const int seg = (tid & 7) * 16;
+    const int tok = t0 + t;
+    const int n = n0 + seg;
+    if (tok < a.m && n < a.n_out) {
+        const float* src = stg + t * ldst + seg;
+        float f[16];
+#pragma unroll
+        for (int i = 0; i < 16; i += 4) {
+            const float4 q = *reinterpret_cast<const float4*>(src + i);
+            f[i] = q.x; f[i + 1] = q.y; f[i + 2] = q.z; f[i + 3] = q.w;
+        }
+        if (a.epi & 1) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) f[i] = fmaxf(f[i], 0.0f);
+        }
+        __nv_bfloat16* dst = a.y + static_cast<int64_t>(tok) * a.ldy + n;
+        const __nv_bfloat16* res = a.res ? a.res + static_cast<int64_t>(tok) * a.ldr + n : nullptr;
+        const bool vec = n + 16 <= a.n_out && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) &&
+                         (!res || (reinterpret_cast<uintptr_t>(res) & 15) == 0);
+        if (vec) {
+            if (res) {
+                const uint4 r0 = *reinterpret_cast<const uint4*>(res);
+                const uint4 r1 = *reinterpret_cast<const uint4*>(res + 8);
+                const __nv_bfloat162* h0 = reinterpret_cast<const __nv_bfloat162*>(&r0);
+                const __nv_bfloat162* h1 = reinterpret_cast<const __nv_bfloat162*>(&r1);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float2 x0 = __bfloat1622float2(h0[i]);
+                    const float2 x1 = __bfloat1622float2(h1[i]);
+                    f[2 * i] += x0.x; f[2 * i + 1] += x0.y;
+                    f[8 + 2 * i] += x1.x; f[8 + 2 * i + 1] += x1.y;
+                }
+            }
+            uint4 o0, o1;
+            o0.x = pack_bf16x2(f[0], f[1]); o0.y = pack_bf16x2(f[2], f[3]);
+            o0.z = pack_bf16x2(f[4], f[5]); o0.w = pack_bf16x2(f[6], f[7]);
+            o1.x = pack_bf16x2(f[8], f[9]); o1.y = pack_bf16x2(f[10], f[11]);
+            o1.z = pack_bf16x2(f[12], f[13]); o1.w = pack_bf16x2(f[14], f[15]);
+            *reinterpret_cast<uint4*>(dst) = o0;
+            *reinterpret_cast<uint4*>(dst + 8) = o1;
+        } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                if (n + i < a.n_out) {
+                    float x = f[i];
+                    if (res) x += __bfloat162float(res[i]);
+                    dst[i] = __float2bfloat16_rn(x);
+                }
+            }
         }
     }
+    asm volatile("bar.sync 2, 128;" ::: "memory");
 }
 
-template <int BITS, bool SYM, int BN, int GPS>
+template <int BITS, bool SYM, int BN, int SPS>
 __global__ void __launch_bounds__(512, 1)
     qgemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const qgemm_args a) {
-    using C = qgemm_cfg<BITS, BN, GPS>;
+    using C = qgemm_cfg<BITS, BN, SPS>;
     constexpr int SS = C::SS, AS = C::AS, NACC = C::NACC;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -183,7 +243,8 @@ __global__ void __launch_bounds__(512, 1)
     auto stage_scale = [&](int s) {
         return reinterpret_cast<float*>(smem + s * C::kStage + C::kB + C::kCodes);
     };
-    constexpr int kScaleRow = 128 * GPS;  // floats: scales of the stage's groups, then zeros
+    constexpr int kScaleRow = 128 * C::NG;  // floats: scales of the stage's groups, then zeros
+    float* stg = reinterpret_cast<float*>(smem + C::kStgOff);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
     uint64_t* full = bars;
     uint64_t* empty = full + SS;
@@ -199,12 +260,14 @@ __global__ void __launch_bounds__(512, 1)
     const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
     const int lane = threadIdx.x & 31;
     long long clk0 = 0;
+#ifdef HP_QGEMM_TRACE
     if (threadIdx.x == 0 && a.trace) {  // per-CTA entry time
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         a.trace[4 * kTraceIters * 4 + 2 * blockIdx.x] = t;
         clk0 = clock64();
     }
+#endif
 
     if (warp == 1 && lane == 0) {
         for (int i = 0; i < SS; ++i) {
@@ -237,23 +300,41 @@ __global__ void __launch_bounds__(512, 1)
         uint32_t it = 0;
         while (iter.next(a, sg)) {
             const int mt = sg.tile / a.NT, nt = sg.tile % a.NT;
-            for (int g = sg.g0; g < sg.g1; g += GPS, ++it) {
-                const int ng = min(GPS, sg.g1 - g);
+            for (int sl = 4 * sg.g0; sl < 4 * sg.g1; sl += SPS, ++it) {
+                const int g = sl >> 2;
+                const int ng = SPS >= 4 ? min(C::NG, sg.g1 - g) : 1;
                 const int s = it % SS;
                 trace_ev(a, 0, it, 0);
                 mbar_wait_warp(&empty[s], ((it / SS) & 1) ^ 1);
                 trace_ev(a, 0, it, 1);
-                const uint32_t cbytes = static_cast<uint32_t>(ng) * BITS * 2048;
+                const size_t t = static_cast<size_t>(nt) * a.G + g;
+                const uint8_t* gsrc = a.packed + t * (BITS * 2048);
+                uint32_t cbytes;
+                if constexpr (SPS >= 4) {
+                    cbytes = static_cast<uint32_t>(ng) * BITS * 2048;
+                } else {
+                    cbytes = C::kCodes;  // half group
+                }
                 const uint32_t sbytes = BITS == 16 ? 0u : static_cast<uint32_t>(ng) * 512u * (SYM ? 1 : 2);
                 mbar_arrive_expect_tx_elect(&full[s], static_cast<uint32_t>(C::kB) + cbytes + sbytes);
-                const size_t t = static_cast<size_t>(nt) * a.G + g;
-                bulk_g2s_elect(stage_codes(s), a.packed + t * (BITS * 2048), cbytes, &full[s]);
+                if constexpr (SPS >= 4) {
+                    bulk_g2s_elect(stage_codes(s), gsrc, cbytes, &full[s]);
+                } else {
+                    const int h = (sl >> 1) & 1;  // which half of the group
+                    if constexpr (BITS == 3) {
+                        // low-2-bit plane of this half + the whole bit-2 plane
+                        bulk_g2s_elect(stage_codes(s), gsrc + h * 2048, 2048, &full[s]);
+                        bulk_g2s_elect(stage_codes(s) + 2048, gsrc + 2 * 2048, 2048, &full[s]);
+                    } else {
+                        bulk_g2s_elect(stage_codes(s), gsrc + h * (BITS * 1024), BITS * 1024, &full[s]);
+                    }
+                }
                 if constexpr (BITS != 16) {
                     bulk_g2s_elect(stage_scale(s), a.scale + t * 128, ng * 512u, &full[s]);
                     if constexpr (!SYM)
                         bulk_g2s_elect(stage_scale(s) + kScaleRow, a.zero + t * 128, ng * 512u, &full[s]);
                 }
-                tma_load_3d_elect(stage_b(s), &tmap_x, 0, mt * BN, g * 2, &full[s]);
+                tma_load_3d_elect(stage_b(s), &tmap_x, 0, mt * BN, sl >> 1, &full[s]);
                 trace_ev(a, 0, it, 2);
             }
         }
@@ -266,8 +347,8 @@ __global__ void __launch_bounds__(512, 1)
             mbar_wait_warp(&tempty[acc], ((ut / NACC) & 1) ^ 1);
             tc_fence_after();
             const uint32_t d_tmem = tmem + acc * BN;
-            for (int g = sg.g0; g < sg.g1; g += GPS, ++it) {
-                const int ng = min(GPS, sg.g1 - g);
+            for (int sl = 4 * sg.g0; sl < 4 * sg.g1; sl += SPS, ++it) {
+                const int nsl = min(SPS, 4 * sg.g1 - sl);
                 const int s = it % SS, as = it % AS;
                 trace_ev(a, 1, it, 0);
                 mbar_wait_warp(&full[s], (it / SS) & 1);
@@ -278,12 +359,12 @@ __global__ void __launch_bounds__(512, 1)
                 const uint32_t bbase = smem_u32(stage_b(s));
                 const uint32_t abase = tmem + C::A0 + as * C::ACOLS;
 #pragma unroll
-                for (int j = 0; j < 8 * GPS; ++j) {
-                    if (j < 8 * ng) {
+                for (int j = 0; j < 2 * SPS; ++j) {
+                    if (j < 2 * nsl) {
                         const uint64_t bdesc =
                             umma_desc_sw128(bbase + (j >> 2) * (BN * 128) + (j & 3) * 32);
                         mma_ts_elect(d_tmem, abase + j * 8, bdesc, idesc,
-                                     (g > sg.g0 || j > 0) ? 1u : 0u);
+                                     (sl > 4 * sg.g0 || j > 0) ? 1u : 0u);
                     }
                 }
                 tc_commit_elect(&empty[s]);
@@ -297,13 +378,14 @@ __global__ void __launch_bounds__(512, 1)
         // ===================== dequant =====================
         const int q = warp - 4;
         const int lq = warp & 3;  // TMEM lane quarter of this warp
-        const int kh = q >> 2;    // warpgroup: slices [kh*2*GPS, (kh+1)*2*GPS) of a stage
+        const int kh = q >> 2;    // warpgroup: local slices [kh*SPS/2, (kh+1)*SPS/2)
         const int r = lq * 32 + lane;
         const uint32_t lane_addr = static_cast<uint32_t>(lq * 32) << 16;
+        constexpr int kSl = SPS / 2;  // slices per warp per stage
         uint32_t it = 0;
         while (iter.next(a, sg)) {
-            for (int g = sg.g0; g < sg.g1; g += GPS, ++it) {
-                const int ng = min(GPS, sg.g1 - g);
+            for (int sl = 4 * sg.g0; sl < 4 * sg.g1; sl += SPS, ++it) {
+                const int nsl = min(SPS, 4 * sg.g1 - sl);
                 const int s = it % SS, as = it % AS;
                 const int trole = (lane == 0 && warp == 4) ? 2 : -1;
                 if (trole >= 0) trace_ev(a, trole, it, 0);
@@ -312,16 +394,28 @@ __global__ void __launch_bounds__(512, 1)
                 mbar_wait(&aempty[as], ((it / AS) & 1) ^ 1);
                 if (trole >= 0) trace_ev(a, trole, it, 2);
                 tc_fence_after();
-                // This warpgroup's share of the stage: GPS == 2 -> group kh (4 slices);
-                // GPS == 1 -> slices 2kh, 2kh+1 of group 0.
-                constexpr int kSl = GPS == 2 ? 4 : 2;
-                const int gi = GPS == 2 ? kh : 0;
-                const int sl0 = GPS == 2 ? 0 : 2 * kh;
-                if (gi < ng) {
-                    const uint32_t sbase = smem_u32(stage_codes(s)) + gi * (BITS * 2048) + r * 16;
+                const int x0 = kh * kSl;  // first local slice of this warp
+                if (x0 < nsl) {
+                    // all local slices of a warp lie in one group (kSl <= 4)
+                    const int gi = x0 >> 2;
+                    const uint32_t cbase = smem_u32(stage_codes(s)) + r * 16;
                     slice_words<BITS> wv[kSl];
 #pragma unroll
-                    for (int h = 0; h < kSl; ++h) load_slice<BITS>(sbase, sl0 + h, wv[h]);
+                    for (int h = 0; h < kSl; ++h) {
+                        const int x = x0 + h;  // local slice in the stage
+                        if constexpr (SPS >= 4) {
+                            load_slice<BITS>(cbase + (x >> 2) * (BITS * 2048), x & 3, wv[h]);
+                        } else if constexpr (BITS == 3) {
+                            // half-group stage: lo plane at chunk 0, bit-2 plane at chunk 1
+                            const int gs = ((sl & 3) + x);  // slice index within the group
+                            const uint2 lo = lds64(cbase + 8 * (gs & 1));
+                            wv[h].w[0] = lo.x;
+                            wv[h].w[1] = lo.y;
+                            wv[h].w[2] = lds32(cbase + 2048 + 4 * gs);
+                        } else {
+                            load_slice<BITS>(cbase, x, wv[h]);
+                        }
+                    }
                     float sf = 0.f, zf = 0.f;
                     if constexpr (BITS != 16) {
                         const uint32_t saddr = smem_u32(stage_scale(s)) + (gi * 128 + r) * 4;
@@ -333,7 +427,7 @@ __global__ void __launch_bounds__(512, 1)
                     for (int h = 0; h < kSl; ++h) {
                         uint32_t v[16];
                         convert_slice<BITS, SYM>(wv[h], sf, zf, s2, z2, v);
-                        tmem_st16(tmem + lane_addr + C::A0 + as * C::ACOLS + gi * 64 + (sl0 + h) * 16, v);
+                        tmem_st16(tmem + lane_addr + C::A0 + as * C::ACOLS + (x0 + h) * 16, v);
                     }
                 }
                 tmem_st_wait();
@@ -352,10 +446,9 @@ __global__ void __launch_bounds__(512, 1)
         while (iter.next(a, sg)) {
             const int mt = sg.tile / a.NT, nt = sg.tile % a.NT;
             const int acc = ut % NACC;
-            const int n = nt * 128 + r;
-            if (threadIdx.x == 384) trace_ev(a, 3, 48 + ut, 0);
+            trace_ev(a, threadIdx.x == 384 ? 3 : 99, 48 + ut, 0);
             mbar_wait(&tfull[acc], (ut / NACC) & 1);
-            if (threadIdx.x == 384) trace_ev(a, 3, 48 + ut, 1);
+            trace_ev(a, threadIdx.x == 384 ? 3 : 99, 48 + ut, 1);
             tc_fence_after();
             constexpr bool kSK = BN <= 64;  // stream-K only runs the decode tiles
             float* part = (kSK && sg.nseg > 1) ? a.partial + ((static_cast<size_t>(sg.tile) * a.maxseg + sg.idx) * 128 + r) * BN
@@ -375,13 +468,13 @@ __global__ void __launch_bounds__(512, 1)
                     float f[16];
 #pragma unroll
                     for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]);
-                    store_out<16>(a, mt * BN + c0, n, f);
+                    stage_store16(a, stg, C::kStgLd, r, f, mt * BN + c0, nt * 128);
                 }
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
-            if (threadIdx.x == 384) trace_ev(a, 3, 48 + ut, 2);
+            trace_ev(a, threadIdx.x == 384 ? 3 : 99, 48 + ut, 2);
 
             if constexpr (kSK) if (sg.nseg > 1) {
                 __threadfence();
@@ -409,23 +502,32 @@ __global__ void __launch_bounds__(512, 1)
                             accv[4 * i + 3] += tmp[i].w;
                         }
                     }
-                    store_out<BN>(a, mt * BN, n, accv);
+#pragma unroll
+                    for (int c0 = 0; c0 < BN; c0 += 16) {
+                        float f[16];
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) f[i] = accv[c0 + i];
+                        stage_store16(a, stg, C::kStgLd, r, f, mt * BN + c0, nt * 128);
+                    }
                     if (warp == 12 && lane == 0) a.counters[sg.tile] = 0u;
                 }
                 asm volatile("bar.sync 1, 128;" ::: "memory");
             }
-            if (threadIdx.x == 384) trace_ev(a, 3, 48 + ut, 3);
+            trace_ev(a, threadIdx.x == 384 ? 3 : 99, 48 + ut, 3);
             ++ut;
         }
     }
 
     __syncthreads();
+#ifdef HP_QGEMM_TRACE
     if (threadIdx.x == 0 && a.trace) {  // per-CTA exit time
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         a.trace[4 * kTraceIters * 4 + 2 * blockIdx.x + 1] = t;
         a.trace[4 * kTraceIters * 4 + 2048 + blockIdx.x] = static_cast<unsigned long long>(clock64() - clk0);
     }
+#endif
+    (void)clk0;
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc<512>(tmem);
@@ -435,12 +537,13 @@ __global__ void __launch_bounds__(512, 1)
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
-// groups of 128 k per pipeline stage: decode tiles move 2 groups per stage to
-// amortise the per-stage barrier/issue work; prefill stages are MMA-heavy.
+// 32-k slices per pipeline stage: decode tiles move two groups per stage to
+// amortise the per-stage barrier/issue work; prefill moves half a group so
+// the [BN x 64] activation tile per stage is small and the pipeline deep.
 template <int BN>
-constexpr int kGroupsPerStage = BN <= 64 ? 2 : 1;
+constexpr int kSlicesPerStage = BN <= 64 ? 8 : 2;
 
-int groups_per_stage(int bn) { return bn <= 64 ? 2 : 1; }
+int slices_per_stage(int bn) { return bn <= 64 ? 8 : 2; }
 
 namespace {
 
@@ -460,17 +563,17 @@ int num_sms() {
 template <int BITS, bool SYM, int BN>
 cudaError_t launch_one(const CUtensorMap& map, const qgemm_args& a, int grid,
                        cudaStream_t st) {
-    constexpr int GPS = kGroupsPerStage<BN>;
-    using C = qgemm_cfg<BITS, BN, GPS>;
+    constexpr int SPS = kSlicesPerStage<BN>;
+    using C = qgemm_cfg<BITS, BN, SPS>;
     static bool attr_done = false;
     if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(qgemm_kernel<BITS, SYM, BN, GPS>,
+        cudaError_t e = cudaFuncSetAttribute(qgemm_kernel<BITS, SYM, BN, SPS>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              C::kSmem);
         if (e != cudaSuccess) return e;
         attr_done = true;
     }
-    qgemm_kernel<BITS, SYM, BN, GPS><<<grid, C::kThreads, C::kSmem, st>>>(map, a);
+    qgemm_kernel<BITS, SYM, BN, SPS><<<grid, C::kThreads, C::kSmem, st>>>(map, a);
     return cudaGetLastError();
 }
 
