@@ -36,7 +36,7 @@ struct qgemm_plan {
     int64_t total;
 };
 qgemm_plan plan_qgemm(int64_t n_out, int64_t k_in, int64_t m, int phase);
-int slices_per_stage(int bn);
+int slices_per_stage(int bits, int bn);
 cudaError_t launch_qgemm(const CUtensorMap& map, const qgemm_plan& p, int bits, bool sym,
                          const void* packed, const float* scale, const float* zero,
                          int64_t n_out, int64_t k_in, int64_t m, void* y, int64_t ldy,
@@ -266,7 +266,7 @@ hp_status hp_qlinear(const hp_qweight* w, const void* x, int64_t ldx, int64_t m,
         return fail(HP_EINVAL, "qlinear: workspace too small (need " +
                                    std::to_string(p.workspace) + " bytes)");
     CUtensorMap map;
-    if (hp_status s = make_act_map(&map, x, w->k_in, m, ldx, p.bn, hp::slices_per_stage(p.bn) / 2))
+    if (hp_status s = make_act_map(&map, x, w->k_in, m, ldx, p.bn, hp::slices_per_stage(w->bits, p.bn) / 2))
         return s;
     return cuda_status(hp::launch_qgemm(map, p, w->bits, w->scheme == HP_SYMMETRIC, w->packed,
                                         w->scale, w->zero, w->n_out, w->k_in, m, y, ldy,

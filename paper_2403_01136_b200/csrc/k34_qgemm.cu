@@ -139,7 +139,13 @@ struct seg_iter {
 // tile per stage small so the pipeline is deep).
 template <int BITS, int BN, int SPS>
 struct qgemm_cfg {
-    static constexpr int kThreads = 512;
+    // decode: 3 dequant warpgroups taking whole stages round-robin (latency
+    // hiding for the ALU/FMA-bound dequant); prefill: 2 warpgroups splitting
+    // each stage's slices.
+    static constexpr int DWG = BN <= 64 ? 3 : 2;
+    static constexpr bool kRR = BN <= 64;
+    static constexpr int kThreads = 128 * (2 + DWG);
+    static constexpr int kEpiWarp0 = 4 + 4 * DWG;
     static constexpr int NG = SPS >= 4 ? SPS / 4 : 1;            // groups touched per stage
     static constexpr int kB = BN * 64 * SPS;                     // SPS/2 64-k swizzled sub-tiles
     static constexpr int kCodes = SPS >= 4 ? BITS * 2048 * NG
@@ -147,20 +153,24 @@ struct qgemm_cfg {
     static constexpr int kScale = BITS == 16 ? 0 : 1024 * NG;    // NG scale rows + NG zero rows
     static constexpr int kStage = kB + kCodes + kScale;
     static constexpr int kBudget = 190 * 1024;
-    static constexpr int SS_ = kBudget / kStage;
-    static constexpr int SS = SS_ > 12 ? 12 : SS_;
+    static constexpr int SS_ = kBudget / kStage > 12 ? 12 : kBudget / kStage;
+    // Round-robin consumers wait only on their own stages, so every ring slot
+    // must always belong to the same warpgroup (depth % DWG == 0); otherwise
+    // an mbarrier parity wait could alias another warpgroup's phase.
+    static constexpr int SS = kRR ? (SS_ / DWG) * DWG : SS_;
     static constexpr int NACC = BN <= 128 ? 2 : 1;
     static constexpr int A0_ = NACC * BN < 64 ? 64 : NACC * BN;
     static constexpr int A0 = (A0_ + 63) / 64 * 64;
     static constexpr int ACOLS = 16 * SPS;                       // TMEM columns per A stage
-    static constexpr int AS_ = (512 - A0) / ACOLS;
-    static constexpr int AS = AS_ > 8 ? 8 : AS_;
+    static constexpr int AS_ = (512 - A0) / ACOLS > 8 ? 8 : (512 - A0) / ACOLS;
+    static constexpr int AS = kRR ? (AS_ / DWG) * DWG : AS_;
     static constexpr int kStgOff = SS * kStage;               // epilogue staging [16][kStgLd] fp32
     static constexpr int kStgLd = 132;
     static constexpr int kBarOff = kStgOff + 16 * kStgLd * 4;
     static constexpr int kSmem = kBarOff + 256 + 1024;  // + barriers + align slack
     static_assert(SS >= 2, "need >= 2 smem stages");
     static_assert(AS >= 2, "need >= 2 TMEM A stages");
+    static_assert(!kRR || (SS % DWG == 0 && AS % DWG == 0), "round-robin ring depth");
     static_assert(SPS == 2 || SPS == 4 || SPS == 8, "SPS");
 };
 
@@ -231,7 +241,7 @@ __device__ __forceinline__ void stage_store16(const qgemm_args& a, float* stg, i
 }
 
 template <int BITS, bool SYM, int BN, int SPS>
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads, 1)
     qgemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const qgemm_args a) {
     using C = qgemm_cfg<BITS, BN, SPS>;
     constexpr int SS = C::SS, AS = C::AS, NACC = C::NACC;
@@ -275,7 +285,7 @@ __global__ void __launch_bounds__(512, 1)
             mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < AS; ++i) {
-            mbar_init(&afull[i], 8);
+            mbar_init(&afull[i], C::kRR ? 4 : 4 * C::DWG);
             mbar_init(&aempty[i], 1);
         }
         for (int i = 0; i < NACC; ++i) {
@@ -374,17 +384,21 @@ __global__ void __launch_bounds__(512, 1)
             tc_commit_elect(&tfull[acc]);
             ++ut;
         }
-    } else if (warp >= 4 && warp < 12) {
+    } else if (warp >= 4 && warp < C::kEpiWarp0) {
         // ===================== dequant =====================
         const int q = warp - 4;
         const int lq = warp & 3;  // TMEM lane quarter of this warp
-        const int kh = q >> 2;    // warpgroup: local slices [kh*SPS/2, (kh+1)*SPS/2)
+        const int wg = q >> 2;    // dequant warpgroup
+        // split mode: this warpgroup's local slices [wg*SPS/2, (wg+1)*SPS/2) of
+        // every stage; round-robin mode: all SPS slices of every DWG-th stage
+        const int kh = C::kRR ? 0 : wg;
         const int r = lq * 32 + lane;
         const uint32_t lane_addr = static_cast<uint32_t>(lq * 32) << 16;
-        constexpr int kSl = SPS / 2;  // slices per warp per stage
+        constexpr int kSl = C::kRR ? SPS : SPS / 2;  // slices per warp per stage
         uint32_t it = 0;
         while (iter.next(a, sg)) {
             for (int sl = 4 * sg.g0; sl < 4 * sg.g1; sl += SPS, ++it) {
+                if (C::kRR && static_cast<int>(it % C::DWG) != wg) continue;
                 const int nsl = min(SPS, 4 * sg.g1 - sl);
                 const int s = it % SS, as = it % AS;
                 const int trole = (lane == 0 && warp == 4) ? 2 : -1;
@@ -396,38 +410,58 @@ __global__ void __launch_bounds__(512, 1)
                 tc_fence_after();
                 const int x0 = kh * kSl;  // first local slice of this warp
                 if (x0 < nsl) {
-                    // all local slices of a warp lie in one group (kSl <= 4)
                     const int gi = x0 >> 2;
                     const uint32_t cbase = smem_u32(stage_codes(s)) + r * 16;
-                    slice_words<BITS> wv[kSl];
+                    // scales of the groups touched by this warp's slices
+                    constexpr int kG = (kSl + 3) / 4;
+                    float sf[kG], zf[kG];
+                    uint32_t s2[kG], z2[kG];
 #pragma unroll
-                    for (int h = 0; h < kSl; ++h) {
-                        const int x = x0 + h;  // local slice in the stage
-                        if constexpr (SPS >= 4) {
-                            load_slice<BITS>(cbase + (x >> 2) * (BITS * 2048), x & 3, wv[h]);
-                        } else if constexpr (BITS == 3) {
-                            // half-group stage: lo plane at chunk 0, bit-2 plane at chunk 1
-                            const int gs = ((sl & 3) + x);  // slice index within the group
-                            const uint2 lo = lds64(cbase + 8 * (gs & 1));
-                            wv[h].w[0] = lo.x;
-                            wv[h].w[1] = lo.y;
-                            wv[h].w[2] = lds32(cbase + 2048 + 4 * gs);
-                        } else {
-                            load_slice<BITS>(cbase, x, wv[h]);
+                    for (int j = 0; j < kG; ++j) {
+                        sf[j] = 0.f;
+                        zf[j] = 0.f;
+                        if constexpr (BITS != 16) {
+                            if (4 * j + x0 < nsl) {
+                                const uint32_t saddr = smem_u32(stage_scale(s)) + ((gi + j) * 128 + r) * 4;
+                                sf[j] = ldsf(saddr);
+                                if constexpr (!SYM) zf[j] = ldsf(saddr + kScaleRow * 4);
+                            }
                         }
+                        s2[j] = bf16x2_splat_bits(sf[j]);
+                        z2[j] = bf16x2_splat_bits(zf[j]);
                     }
-                    float sf = 0.f, zf = 0.f;
-                    if constexpr (BITS != 16) {
-                        const uint32_t saddr = smem_u32(stage_scale(s)) + (gi * 128 + r) * 4;
-                        sf = ldsf(saddr);
-                        if constexpr (!SYM) zf = ldsf(saddr + kScaleRow * 4);
-                    }
-                    const uint32_t s2 = bf16x2_splat_bits(sf), z2 = bf16x2_splat_bits(zf);
+                    // batches of <= 4 slices: load words, then convert + store
+                    constexpr int kB4 = kSl < 4 ? kSl : 4;
 #pragma unroll
-                    for (int h = 0; h < kSl; ++h) {
-                        uint32_t v[16];
-                        convert_slice<BITS, SYM>(wv[h], sf, zf, s2, z2, v);
-                        tmem_st16(tmem + lane_addr + C::A0 + as * C::ACOLS + (x0 + h) * 16, v);
+                    for (int hb = 0; hb < kSl; hb += kB4) {
+                        slice_words<BITS> wv[kB4];
+#pragma unroll
+                        for (int hh = 0; hh < kB4; ++hh) {
+                            const int x = x0 + hb + hh;  // local slice in the stage
+                            if (x >= nsl) continue;
+                            if constexpr (SPS >= 4) {
+                                load_slice<BITS>(cbase + (x >> 2) * (BITS * 2048), x & 3, wv[hh]);
+                            } else if constexpr (BITS == 3) {
+                                // half-group stage: lo plane at chunk 0, bit-2 plane at chunk 1
+                                const int gs = ((sl & 3) + x);  // slice index within the group
+                                const uint2 lo = lds64(cbase + 8 * (gs & 1));
+                                wv[hh].w[0] = lo.x;
+                                wv[hh].w[1] = lo.y;
+                                wv[hh].w[2] = lds32(cbase + 2048 + 4 * gs);
+                            } else {
+                                load_slice<BITS>(cbase, x, wv[hh]);
+                            }
+                        }
+#pragma unroll
+                        for (int hh = 0; hh < kB4; ++hh) {
+                            const int h = hb + hh;
+                            if (x0 + h < nsl) {
+                                const int j = h >> 2;
+                                uint32_t v[16];
+                                convert_slice<BITS, SYM>(wv[hh], sf[j], zf[j], s2[j], z2[j], v);
+                                tmem_st16(tmem + lane_addr + C::A0 + as * C::ACOLS + (x0 + h) * 16, v);
+                            }
+                        }
                     }
                 }
                 tmem_st_wait();
@@ -437,7 +471,7 @@ __global__ void __launch_bounds__(512, 1)
                 if (trole >= 0) trace_ev(a, trole, it, 3);
             }
         }
-    } else if (warp >= 12) {
+    } else if (warp >= C::kEpiWarp0) {
         // ===================== epilogue =====================
         const int lq = warp & 3;
         const int r = lq * 32 + lane;
@@ -446,9 +480,9 @@ __global__ void __launch_bounds__(512, 1)
         while (iter.next(a, sg)) {
             const int mt = sg.tile / a.NT, nt = sg.tile % a.NT;
             const int acc = ut % NACC;
-            trace_ev(a, threadIdx.x == 384 ? 3 : 99, 48 + ut, 0);
+            trace_ev(a, warp == C::kEpiWarp0 && lane == 0 ? 3 : 99, 48 + ut, 0);
             mbar_wait(&tfull[acc], (ut / NACC) & 1);
-            trace_ev(a, threadIdx.x == 384 ? 3 : 99, 48 + ut, 1);
+            trace_ev(a, warp == C::kEpiWarp0 && lane == 0 ? 3 : 99, 48 + ut, 1);
             tc_fence_after();
             constexpr bool kSK = BN <= 64;  // stream-K only runs the decode tiles
             float* part = (kSK && sg.nseg > 1) ? a.partial + ((static_cast<size_t>(sg.tile) * a.maxseg + sg.idx) * 128 + r) * BN
@@ -474,12 +508,12 @@ __global__ void __launch_bounds__(512, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
-            trace_ev(a, threadIdx.x == 384 ? 3 : 99, 48 + ut, 2);
+            trace_ev(a, warp == C::kEpiWarp0 && lane == 0 ? 3 : 99, 48 + ut, 2);
 
             if constexpr (kSK) if (sg.nseg > 1) {
                 __threadfence();
                 asm volatile("bar.sync 1, 128;" ::: "memory");
-                if (warp == 12 && lane == 0)
+                if (warp == C::kEpiWarp0 && lane == 0)
                     *bcast = atomicAdd(&a.counters[sg.tile], 1u);
                 asm volatile("bar.sync 1, 128;" ::: "memory");
                 if (*bcast == static_cast<unsigned>(sg.nseg - 1)) {
@@ -509,11 +543,11 @@ __global__ void __launch_bounds__(512, 1)
                         for (int i = 0; i < 16; ++i) f[i] = accv[c0 + i];
                         stage_store16(a, stg, C::kStgLd, r, f, mt * BN + c0, nt * 128);
                     }
-                    if (warp == 12 && lane == 0) a.counters[sg.tile] = 0u;
+                    if (warp == C::kEpiWarp0 && lane == 0) a.counters[sg.tile] = 0u;
                 }
                 asm volatile("bar.sync 1, 128;" ::: "memory");
             }
-            trace_ev(a, threadIdx.x == 384 ? 3 : 99, 48 + ut, 3);
+            trace_ev(a, warp == C::kEpiWarp0 && lane == 0 ? 3 : 99, 48 + ut, 3);
             ++ut;
         }
     }
@@ -540,10 +574,10 @@ __global__ void __launch_bounds__(512, 1)
 // 32-k slices per pipeline stage: decode tiles move two groups per stage to
 // amortise the per-stage barrier/issue work; prefill moves half a group so
 // the [BN x 64] activation tile per stage is small and the pipeline deep.
-template <int BN>
-constexpr int kSlicesPerStage = BN <= 64 ? 8 : 2;
+template <int BITS, int BN>
+constexpr int kSlicesPerStage = BN <= 64 ? (BITS == 16 ? 4 : 8) : 2;
 
-int slices_per_stage(int bn) { return bn <= 64 ? 8 : 2; }
+int slices_per_stage(int bits, int bn) { return bn <= 64 ? (bits == 16 ? 4 : 8) : 2; }
 
 namespace {
 
@@ -563,7 +597,7 @@ int num_sms() {
 template <int BITS, bool SYM, int BN>
 cudaError_t launch_one(const CUtensorMap& map, const qgemm_args& a, int grid,
                        cudaStream_t st) {
-    constexpr int SPS = kSlicesPerStage<BN>;
+    constexpr int SPS = kSlicesPerStage<BITS, BN>;
     using C = qgemm_cfg<BITS, BN, SPS>;
     static bool attr_done = false;
     if (!attr_done) {
