@@ -139,11 +139,11 @@ struct seg_iter {
 // tile per stage small so the pipeline is deep).
 template <int BITS, int BN, int SPS>
 struct qgemm_cfg {
-    // decode: 3 dequant warpgroups taking whole stages round-robin (latency
-    // hiding for the ALU/FMA-bound dequant); prefill: 2 warpgroups splitting
-    // each stage's slices.
-    static constexpr int DWG = BN <= 64 ? 3 : 2;
-    static constexpr bool kRR = BN <= 64;
+    // Dequant warpgroups: decode 3/4/8-bit use 3 warpgroups taking whole
+    // stages round-robin (latency hiding for the ALU/FMA-bound dequant);
+    // prefill and 16-bit decode use 2 warpgroups splitting every stage.
+    static constexpr bool kRR = BN <= 64 && BITS != 16;
+    static constexpr int DWG = kRR ? 3 : 2;
     static constexpr int kThreads = 128 * (2 + DWG);
     static constexpr int kEpiWarp0 = 4 + 4 * DWG;
     static constexpr int NG = SPS >= 4 ? SPS / 4 : 1;            // groups touched per stage
@@ -151,27 +151,34 @@ struct qgemm_cfg {
     static constexpr int kCodes = SPS >= 4 ? BITS * 2048 * NG
                                            : (BITS == 3 ? 4096 : BITS * 1024);  // half group
     static constexpr int kScale = BITS == 16 ? 0 : 1024 * NG;    // NG scale rows + NG zero rows
-    static constexpr int kStage = kB + kCodes + kScale;
-    static constexpr int kBudget = 190 * 1024;
-    static constexpr int SS_ = kBudget / kStage > 12 ? 12 : kBudget / kStage;
+    static constexpr int kCS = kCodes + kScale;                  // weight-ring slot
+    // Two rings: the weight-code ring (HBM latency, released as soon as the
+    // dequant warps hold the codes in registers) is deep; the activation
+    // ring (L2-resident x, released by the MMA) is shallow.
+    static constexpr int kBudget = 186 * 1024;
+    static constexpr int BR = BN <= 64 ? 3 : (BN <= 128 ? 6 : 4);
+    static constexpr int CR_ = (kBudget - BR * kB) / kCS > 12 ? 12 : (kBudget - BR * kB) / kCS;
     // Round-robin consumers wait only on their own stages, so every ring slot
-    // must always belong to the same warpgroup (depth % DWG == 0); otherwise
-    // an mbarrier parity wait could alias another warpgroup's phase.
-    static constexpr int SS = kRR ? (SS_ / DWG) * DWG : SS_;
+    // they consume must always belong to the same warpgroup (depth % DWG ==
+    // 0); otherwise an mbarrier parity wait could alias another phase.
+    static constexpr int CR = kRR ? (CR_ / DWG) * DWG : CR_;
     static constexpr int NACC = BN <= 128 ? 2 : 1;
     static constexpr int A0_ = NACC * BN < 64 ? 64 : NACC * BN;
     static constexpr int A0 = (A0_ + 63) / 64 * 64;
     static constexpr int ACOLS = 16 * SPS;                       // TMEM columns per A stage
     static constexpr int AS_ = (512 - A0) / ACOLS > 8 ? 8 : (512 - A0) / ACOLS;
     static constexpr int AS = kRR ? (AS_ / DWG) * DWG : AS_;
-    static constexpr int kStgOff = SS * kStage;               // epilogue staging [16][kStgLd] fp32
+    static constexpr int kCodesOff = BR * kB;                    // B ring first (1024-aligned)
+    static constexpr int kStgOff = kCodesOff + CR * kCS;         // epilogue staging [16][kStgLd] fp32
     static constexpr int kStgLd = 132;
     static constexpr int kBarOff = kStgOff + 16 * kStgLd * 4;
-    static constexpr int kSmem = kBarOff + 256 + 1024;  // + barriers + align slack
-    static_assert(SS >= 2, "need >= 2 smem stages");
+    static constexpr int kSmem = kBarOff + 512 + 1024;  // + barriers + align slack
+    static constexpr int kEmptyC = kRR ? 4 : 4 * DWG;            // dequant warps per stage
+    static_assert(CR >= 2 && BR >= 2, "need >= 2 ring slots");
     static_assert(AS >= 2, "need >= 2 TMEM A stages");
-    static_assert(!kRR || (SS % DWG == 0 && AS % DWG == 0), "round-robin ring depth");
+    static_assert(!kRR || (CR % DWG == 0 && AS % DWG == 0), "round-robin ring depth");
     static_assert(SPS == 2 || SPS == 4 || SPS == 8, "SPS");
+    static_assert(kSmem <= 227 * 1024, "smem");
 };
 
 // Epilogue write-out of 16 tokens x 128 rows through shared memory: each
@@ -244,21 +251,24 @@ template <int BITS, bool SYM, int BN, int SPS>
 __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads, 1)
     qgemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const qgemm_args a) {
     using C = qgemm_cfg<BITS, BN, SPS>;
-    constexpr int SS = C::SS, AS = C::AS, NACC = C::NACC;
+    constexpr int AS = C::AS, NACC = C::NACC;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    auto stage_b = [&](int s) { return smem + s * C::kStage; };
-    auto stage_codes = [&](int s) { return smem + s * C::kStage + C::kB; };
+    auto stage_b = [&](int s) { return smem + s * C::kB; };
+    auto stage_codes = [&](int s) { return smem + C::kCodesOff + s * C::kCS; };
     auto stage_scale = [&](int s) {
-        return reinterpret_cast<float*>(smem + s * C::kStage + C::kB + C::kCodes);
+        return reinterpret_cast<float*>(smem + C::kCodesOff + s * C::kCS + C::kCodes);
     };
     constexpr int kScaleRow = 128 * C::NG;  // floats: scales of the stage's groups, then zeros
+    constexpr int CR = C::CR, BR = C::BR;
     float* stg = reinterpret_cast<float*>(smem + C::kStgOff);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
-    uint64_t* full = bars;
-    uint64_t* empty = full + SS;
-    uint64_t* afull = empty + SS;
+    uint64_t* full_c = bars;
+    uint64_t* empty_c = full_c + CR;
+    uint64_t* full_b = empty_c + CR;
+    uint64_t* empty_b = full_b + BR;
+    uint64_t* afull = empty_b + BR;
     uint64_t* aempty = afull + AS;
     uint64_t* tfull = aempty + AS;
     uint64_t* tempty = tfull + NACC;
@@ -280,9 +290,13 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads, 1)
 #endif
 
     if (warp == 1 && lane == 0) {
-        for (int i = 0; i < SS; ++i) {
-            mbar_init(&full[i], 1);
-            mbar_init(&empty[i], 1);
+        for (int i = 0; i < CR; ++i) {
+            mbar_init(&full_c[i], 1);
+            mbar_init(&empty_c[i], C::kEmptyC);
+        }
+        for (int i = 0; i < BR; ++i) {
+            mbar_init(&full_b[i], 1);
+            mbar_init(&empty_b[i], 1);
         }
         for (int i = 0; i < AS; ++i) {
             mbar_init(&afull[i], C::kRR ? 4 : 4 * C::DWG);
@@ -294,7 +308,7 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads, 1)
         }
         fence_mbar_init();
     }
-    if (warp == 0 && lane == 0) prefetch_tmap(&tmap_x);
+    if (warp == 3 && lane == 0) prefetch_tmap(&tmap_x);
     if (warp == 2) tmem_alloc<512>(tmem_slot);
     tc_fence_before();
     __syncthreads();
@@ -306,46 +320,53 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads, 1)
     seg_t sg;
 
     if (warp == 0) {
-        // ===================== producer (whole warp, elected issue) ============
+        // ============ weight-code producer (whole warp, elected issue) ==========
         uint32_t it = 0;
         while (iter.next(a, sg)) {
-            const int mt = sg.tile / a.NT, nt = sg.tile % a.NT;
+            const int nt = sg.tile % a.NT;
             for (int sl = 4 * sg.g0; sl < 4 * sg.g1; sl += SPS, ++it) {
                 const int g = sl >> 2;
                 const int ng = SPS >= 4 ? min(C::NG, sg.g1 - g) : 1;
-                const int s = it % SS;
+                const int s = it % CR;
                 trace_ev(a, 0, it, 0);
-                mbar_wait_warp(&empty[s], ((it / SS) & 1) ^ 1);
+                mbar_wait_warp(&empty_c[s], ((it / CR) & 1) ^ 1);
                 trace_ev(a, 0, it, 1);
                 const size_t t = static_cast<size_t>(nt) * a.G + g;
                 const uint8_t* gsrc = a.packed + t * (BITS * 2048);
-                uint32_t cbytes;
-                if constexpr (SPS >= 4) {
-                    cbytes = static_cast<uint32_t>(ng) * BITS * 2048;
-                } else {
-                    cbytes = C::kCodes;  // half group
-                }
+                const uint32_t cbytes = SPS >= 4 ? static_cast<uint32_t>(ng) * BITS * 2048
+                                                 : static_cast<uint32_t>(C::kCodes);
                 const uint32_t sbytes = BITS == 16 ? 0u : static_cast<uint32_t>(ng) * 512u * (SYM ? 1 : 2);
-                mbar_arrive_expect_tx_elect(&full[s], static_cast<uint32_t>(C::kB) + cbytes + sbytes);
+                mbar_arrive_expect_tx_elect(&full_c[s], cbytes + sbytes);
                 if constexpr (SPS >= 4) {
-                    bulk_g2s_elect(stage_codes(s), gsrc, cbytes, &full[s]);
+                    bulk_g2s_elect(stage_codes(s), gsrc, cbytes, &full_c[s]);
                 } else {
                     const int h = (sl >> 1) & 1;  // which half of the group
                     if constexpr (BITS == 3) {
                         // low-2-bit plane of this half + the whole bit-2 plane
-                        bulk_g2s_elect(stage_codes(s), gsrc + h * 2048, 2048, &full[s]);
-                        bulk_g2s_elect(stage_codes(s) + 2048, gsrc + 2 * 2048, 2048, &full[s]);
+                        bulk_g2s_elect(stage_codes(s), gsrc + h * 2048, 2048, &full_c[s]);
+                        bulk_g2s_elect(stage_codes(s) + 2048, gsrc + 2 * 2048, 2048, &full_c[s]);
                     } else {
-                        bulk_g2s_elect(stage_codes(s), gsrc + h * (BITS * 1024), BITS * 1024, &full[s]);
+                        bulk_g2s_elect(stage_codes(s), gsrc + h * (BITS * 1024), BITS * 1024, &full_c[s]);
                     }
                 }
                 if constexpr (BITS != 16) {
-                    bulk_g2s_elect(stage_scale(s), a.scale + t * 128, ng * 512u, &full[s]);
+                    bulk_g2s_elect(stage_scale(s), a.scale + t * 128, ng * 512u, &full_c[s]);
                     if constexpr (!SYM)
-                        bulk_g2s_elect(stage_scale(s) + kScaleRow, a.zero + t * 128, ng * 512u, &full[s]);
+                        bulk_g2s_elect(stage_scale(s) + kScaleRow, a.zero + t * 128, ng * 512u, &full_c[s]);
                 }
-                tma_load_3d_elect(stage_b(s), &tmap_x, 0, mt * BN, sl >> 1, &full[s]);
                 trace_ev(a, 0, it, 2);
+            }
+        }
+    } else if (warp == 3) {
+        // ============ activation producer (whole warp, elected issue) ===========
+        uint32_t it = 0;
+        while (iter.next(a, sg)) {
+            const int mt = sg.tile / a.NT;
+            for (int sl = 4 * sg.g0; sl < 4 * sg.g1; sl += SPS, ++it) {
+                const int s = it % BR;
+                mbar_wait_warp(&empty_b[s], ((it / BR) & 1) ^ 1);
+                mbar_arrive_expect_tx_elect(&full_b[s], static_cast<uint32_t>(C::kB));
+                tma_load_3d_elect(stage_b(s), &tmap_x, 0, mt * BN, sl >> 1, &full_b[s]);
             }
         }
     } else if (warp == 1) {
@@ -359,9 +380,9 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads, 1)
             const uint32_t d_tmem = tmem + acc * BN;
             for (int sl = 4 * sg.g0; sl < 4 * sg.g1; sl += SPS, ++it) {
                 const int nsl = min(SPS, 4 * sg.g1 - sl);
-                const int s = it % SS, as = it % AS;
+                const int s = it % BR, as = it % AS;
                 trace_ev(a, 1, it, 0);
-                mbar_wait_warp(&full[s], (it / SS) & 1);
+                mbar_wait_warp(&full_b[s], (it / BR) & 1);
                 trace_ev(a, 1, it, 1);
                 mbar_wait_warp(&afull[as], (it / AS) & 1);
                 trace_ev(a, 1, it, 2);
@@ -377,7 +398,7 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads, 1)
                                      (sl > 4 * sg.g0 || j > 0) ? 1u : 0u);
                     }
                 }
-                tc_commit_elect(&empty[s]);
+                tc_commit_elect(&empty_b[s]);
                 tc_commit_elect(&aempty[as]);
                 trace_ev(a, 1, it, 3);
             }
@@ -400,68 +421,62 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads, 1)
             for (int sl = 4 * sg.g0; sl < 4 * sg.g1; sl += SPS, ++it) {
                 if (C::kRR && static_cast<int>(it % C::DWG) != wg) continue;
                 const int nsl = min(SPS, 4 * sg.g1 - sl);
-                const int s = it % SS, as = it % AS;
+                const int s = it % CR, as = it % AS;
                 const int trole = (lane == 0 && warp == 4) ? 2 : -1;
                 if (trole >= 0) trace_ev(a, trole, it, 0);
-                mbar_wait(&full[s], (it / SS) & 1);
+                mbar_wait(&full_c[s], (it / CR) & 1);
                 if (trole >= 0) trace_ev(a, trole, it, 1);
                 mbar_wait(&aempty[as], ((it / AS) & 1) ^ 1);
                 if (trole >= 0) trace_ev(a, trole, it, 2);
                 tc_fence_after();
                 const int x0 = kh * kSl;  // first local slice of this warp
-                if (x0 < nsl) {
-                    const int gi = x0 >> 2;
-                    const uint32_t cbase = smem_u32(stage_codes(s)) + r * 16;
-                    // scales of the groups touched by this warp's slices
-                    constexpr int kG = (kSl + 3) / 4;
-                    float sf[kG], zf[kG];
-                    uint32_t s2[kG], z2[kG];
+                const int gi = x0 >> 2;
+                const uint32_t cbase = smem_u32(stage_codes(s)) + r * 16;
+                // phase 1: this warp's codes and scales into registers ...
+                constexpr int kG = (kSl + 3) / 4;  // groups touched by the warp's slices
+                float sf[kG], zf[kG];
+                slice_words<BITS> wv[kSl];
 #pragma unroll
-                    for (int j = 0; j < kG; ++j) {
-                        sf[j] = 0.f;
-                        zf[j] = 0.f;
-                        if constexpr (BITS != 16) {
-                            if (4 * j + x0 < nsl) {
-                                const uint32_t saddr = smem_u32(stage_scale(s)) + ((gi + j) * 128 + r) * 4;
-                                sf[j] = ldsf(saddr);
-                                if constexpr (!SYM) zf[j] = ldsf(saddr + kScaleRow * 4);
-                            }
+                for (int j = 0; j < kG; ++j) {
+                    sf[j] = 0.f;
+                    zf[j] = 0.f;
+                    if constexpr (BITS != 16) {
+                        if (4 * j + x0 < nsl) {
+                            const uint32_t saddr = smem_u32(stage_scale(s)) + ((gi + j) * 128 + r) * 4;
+                            sf[j] = ldsf(saddr);
+                            if constexpr (!SYM) zf[j] = ldsf(saddr + kScaleRow * 4);
                         }
-                        s2[j] = bf16x2_splat_bits(sf[j]);
-                        z2[j] = bf16x2_splat_bits(zf[j]);
                     }
-                    // batches of <= 4 slices: load words, then convert + store
-                    constexpr int kB4 = kSl < 4 ? kSl : 4;
+                }
 #pragma unroll
-                    for (int hb = 0; hb < kSl; hb += kB4) {
-                        slice_words<BITS> wv[kB4];
+                for (int h = 0; h < kSl; ++h) {
+                    const int x = x0 + h;  // local slice in the stage
+                    if (x >= nsl) continue;
+                    if constexpr (SPS >= 4) {
+                        load_slice<BITS>(cbase + (x >> 2) * (BITS * 2048), x & 3, wv[h]);
+                    } else if constexpr (BITS == 3) {
+                        // half-group stage: lo plane at chunk 0, bit-2 plane at chunk 1
+                        const int gs = ((sl & 3) + x);  // slice index within the group
+                        const uint2 lo = lds64(cbase + 8 * (gs & 1));
+                        wv[h].w[0] = lo.x;
+                        wv[h].w[1] = lo.y;
+                        wv[h].w[2] = lds32(cbase + 2048 + 4 * gs);
+                    } else {
+                        load_slice<BITS>(cbase, x, wv[h]);
+                    }
+                }
+                // ... then hand the weight slot back to the producer at once
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty_c[s]);
+                // phase 2: convert + store into the TMEM A stage
 #pragma unroll
-                        for (int hh = 0; hh < kB4; ++hh) {
-                            const int x = x0 + hb + hh;  // local slice in the stage
-                            if (x >= nsl) continue;
-                            if constexpr (SPS >= 4) {
-                                load_slice<BITS>(cbase + (x >> 2) * (BITS * 2048), x & 3, wv[hh]);
-                            } else if constexpr (BITS == 3) {
-                                // half-group stage: lo plane at chunk 0, bit-2 plane at chunk 1
-                                const int gs = ((sl & 3) + x);  // slice index within the group
-                                const uint2 lo = lds64(cbase + 8 * (gs & 1));
-                                wv[hh].w[0] = lo.x;
-                                wv[hh].w[1] = lo.y;
-                                wv[hh].w[2] = lds32(cbase + 2048 + 4 * gs);
-                            } else {
-                                load_slice<BITS>(cbase, x, wv[hh]);
-                            }
-                        }
-#pragma unroll
-                        for (int hh = 0; hh < kB4; ++hh) {
-                            const int h = hb + hh;
-                            if (x0 + h < nsl) {
-                                const int j = h >> 2;
-                                uint32_t v[16];
-                                convert_slice<BITS, SYM>(wv[hh], sf[j], zf[j], s2[j], z2[j], v);
-                                tmem_st16(tmem + lane_addr + C::A0 + as * C::ACOLS + (x0 + h) * 16, v);
-                            }
-                        }
+                for (int h = 0; h < kSl; ++h) {
+                    if (x0 + h < nsl) {
+                        const int j = h >> 2;
+                        uint32_t v[16];
+                        convert_slice<BITS, SYM>(wv[h], sf[j], zf[j], bf16x2_splat_bits(sf[j]),
+                                                 bf16x2_splat_bits(zf[j]), v);
+                        tmem_st16(tmem + lane_addr + C::A0 + as * C::ACOLS + (x0 + h) * 16, v);
                     }
                 }
                 tmem_st_wait();
@@ -559,6 +574,9 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads, 1)
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         a.trace[4 * kTraceIters * 4 + 2 * blockIdx.x + 1] = t;
         a.trace[4 * kTraceIters * 4 + 2048 + blockIdx.x] = static_cast<unsigned long long>(clock64() - clk0);
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        a.trace[4 * kTraceIters * 4 + 3072 + blockIdx.x] = smid;
     }
 #endif
     (void)clk0;
@@ -575,9 +593,9 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads, 1)
 // amortise the per-stage barrier/issue work; prefill moves half a group so
 // the [BN x 64] activation tile per stage is small and the pipeline deep.
 template <int BITS, int BN>
-constexpr int kSlicesPerStage = BN <= 64 ? (BITS == 16 ? 4 : 8) : 2;
+constexpr int kSlicesPerStage = BN <= 64 ? (BITS >= 8 ? 4 : 8) : 2;
 
-int slices_per_stage(int bits, int bn) { return bn <= 64 ? (bits == 16 ? 4 : 8) : 2; }
+int slices_per_stage(int bits, int bn) { return bn <= 64 ? (bits >= 8 ? 4 : 8) : 2; }
 
 namespace {
 
@@ -674,8 +692,8 @@ unsigned long long* trace_buffer() {
         if (getenv("HP_QGEMM_TRACE")) {
             int cta = getenv("HP_QGEMM_TRACE_CTA") ? atoi(getenv("HP_QGEMM_TRACE_CTA")) : 0;
             cudaMemcpyToSymbol(g_trace_cta, &cta, sizeof(int));
-            cudaMalloc(&g_trace, sizeof(unsigned long long) * (4 * kTraceIters * 4 + 3 * 1024));
-            cudaMemset(g_trace, 0, sizeof(unsigned long long) * (4 * kTraceIters * 4 + 3 * 1024));
+            cudaMalloc(&g_trace, sizeof(unsigned long long) * (4 * kTraceIters * 4 + 4 * 1024));
+            cudaMemset(g_trace, 0, sizeof(unsigned long long) * (4 * kTraceIters * 4 + 4 * 1024));
         }
     }
     return g_trace;

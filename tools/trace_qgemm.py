@@ -22,7 +22,7 @@ def main():
     for _ in range(3):
         qweight.qlinear(qw, x, phase=1)
     torch.cuda.synchronize()
-    buf = np.zeros(4 * 64 * 4 + 3 * 1024, dtype=np.uint64)
+    buf = np.zeros(4 * 64 * 4 + 4 * 1024, dtype=np.uint64)
     lib.hp_debug_trace(buf.ctypes.data, buf.size)
     cyc = buf[4 * 64 * 4 + 2048:4 * 64 * 4 + 2048 + 148].astype(np.int64)
     cta = buf[4 * 64 * 4:4 * 64 * 4 + 2048].reshape(1024, 2).astype(np.int64)
@@ -33,6 +33,9 @@ def main():
     print(f"CTAs {len(cta)}: entry min/med/max {ent.min():.2f}/{np.median(ent):.2f}/{ent.max():.2f} us; "
           f"exit min/med/max {ext.min():.2f}/{np.median(ext):.2f}/{ext.max():.2f} us")
     print("  exit sorted (last 10):", np.round(np.sort(ext)[-10:], 2), " argmax", int(np.argmax(ext)))
+    print("  exit by CTA:", " ".join(f"{v:.1f}" for v in ext))
+    smid = buf[4 * 64 * 4 + 2048 + 1024:4 * 64 * 4 + 2048 + 1024 + 148].astype(np.int64)
+    print("  smid by CTA:", " ".join(str(v) for v in smid))
     span_ns = (cta[:148, 1] - cta[:148, 0]).astype(np.float64)
     print(f"  CTA cycles/ns (implied GHz): median {np.median(cyc / span_ns):.3f}, cycles median {np.median(cyc):.0f}")
     g = torch.cuda.CUDAGraph()
