@@ -50,6 +50,10 @@ int hp_device_ok(void);
 /* Cap the persistent K3/K4 grid at `sms` CTAs (0 = every SM), leaving SMs
  * to NCCL kernels that run concurrently in pipeline mode.               */
 void hp_set_sm_budget(int sms);
+/* Programmatic dependent launch between consecutive K3/K4/glue kernels on a
+ * stream (default on): the next kernel's prologue and weight streaming
+ * overlap the previous kernel's tail; its activation reads wait.        */
+void hp_set_pdl(int enable);
 
 /* Quantizer scheme / rounding — numeric values match the order of
  * hetplan::indicator::quant_scheme / rounding_mode (indicator.hpp:22-23). */

@@ -91,6 +91,7 @@ def _load() -> C.CDLL:
     }
     sig.update({
         "hp_set_sm_budget": (None, [i32]),
+        "hp_set_pdl": (None, [i32]),
         "hp_nccl_unique_id": (i32, [v]),
         "hp_pipeline_create": (i32, [p, p, i32, i32, v, P(hp_pipeline_options), P(v)]),
         "hp_pipeline_run": (i32, [v, v, v, P(d)]),
@@ -118,7 +119,7 @@ EXPORTED = [
     "hp_quant_pack", "hp_quant_unpack", "hp_dequant", "hp_indicator_stats",
     "hp_qlinear_workspace_bytes", "hp_qlinear", "hp_host_scaling_factor", "hp_host_g_of_x",
     "hp_host_indicator_csv", "hp_host_omega_from_stats", "hp_host_memcost", "hp_host_preset",
-    "hp_host_make_schedule", "hp_host_simulate", "hp_host_plan_check", "hp_set_sm_budget",
+    "hp_host_make_schedule", "hp_host_simulate", "hp_host_plan_check", "hp_set_sm_budget", "hp_set_pdl",
     "hp_nccl_unique_id", "hp_pipeline_create", "hp_pipeline_run", "hp_pipeline_stage_costs",
     "hp_pipeline_kernel_stats", "hp_pipeline_info", "hp_pipeline_destroy",
 ]

@@ -15,6 +15,7 @@
 
 namespace hp {
 extern int g_sm_budget;
+extern int g_pdl;
 extern unsigned long long* g_trace;
 cudaError_t launch_quant_pack(const void* w, int64_t n_out, int64_t k_in, int64_t ldw,
                               int bits, int sym, void* packed, float* scale, float* zero,
@@ -158,6 +159,8 @@ int hp_abi_version(void) { return 1; }
 int hp_device_ok(void) { return device_ok_cached(); }
 
 void hp_set_sm_budget(int sms) { hp::g_sm_budget = sms > 0 ? sms : 0; }
+
+void hp_set_pdl(int enable) { hp::g_pdl = enable ? 1 : 0; }
 
 /* debug: copy the HP_QGEMM_TRACE clock trace (4 roles x 64 iters x 4 events) */
 int hp_debug_trace(unsigned long long* host, int n) {

@@ -40,6 +40,8 @@ __global__ void __launch_bounds__(kThreads)
                      __nv_bfloat16* __restrict__ y, int64_t ldy) {
     constexpr int kMaxPer = 64;  // h <= 64 * kThreads
     __shared__ float red[kThreads / 32];
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const __nv_bfloat16* xr = x + blockIdx.x * ldx;
     __nv_bfloat16* yr = y + blockIdx.x * ldy;
     float v[kMaxPer];
@@ -86,6 +88,7 @@ __global__ void __launch_bounds__(kThreads)
 __global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ src, int64_t lds,
                                    int64_t stride, int64_t offset, int rows, int h,
                                    __nv_bfloat16* __restrict__ dst, int64_t ldd) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int r = blockIdx.x;
     const __nv_bfloat16* s = src + (static_cast<int64_t>(r) * stride + offset) * lds;
     for (int c = threadIdx.x; c < h; c += blockDim.x) dst[r * ldd + c] = s[c];
@@ -105,10 +108,20 @@ cudaError_t launch_synth(void* out, int64_t n, uint64_t seed, double mean, doubl
 cudaError_t launch_layernorm(const void* x, int64_t ldx, int64_t rows, int h, const void* gamma,
                              const void* beta, void* y, int64_t ldy, cudaStream_t st) {
     if (h > 64 * 256) return cudaErrorInvalidValue;
-    layernorm_kernel<256><<<static_cast<unsigned>(rows), 256, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(x), ldx, h, static_cast<const __nv_bfloat16*>(gamma),
-        static_cast<const __nv_bfloat16*>(beta), static_cast<__nv_bfloat16*>(y), ldy);
-    return cudaGetLastError();
+    extern int g_pdl;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(rows));
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, layernorm_kernel<256>, static_cast<const __nv_bfloat16*>(x), ldx,
+                              h, static_cast<const __nv_bfloat16*>(gamma),
+                              static_cast<const __nv_bfloat16*>(beta),
+                              static_cast<__nv_bfloat16*>(y), ldy);
 }
 
 cudaError_t launch_gather_rows(const void* src, int64_t lds, int64_t stride, int64_t offset,

@@ -35,6 +35,8 @@ namespace hp {
 
 // Persistent-grid cap: leave SMs to concurrent NCCL kernels (pipeline runs).
 int g_sm_budget = 0;
+// Programmatic dependent launch for qgemm / glue kernels (hp_set_pdl).
+int g_pdl = 1;
 
 struct qgemm_args {
     const uint8_t* packed;
@@ -314,6 +316,9 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform
+    // PDL: the next kernel may launch now; everything that reads the previous
+    // kernel's outputs (x, residual, split-K workspace) waits in pdl_wait().
+    pdl_trigger();
 
     seg_iter iter;
     iter.init(a);
@@ -359,6 +364,7 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads, 1)
         }
     } else if (warp == 3) {
         // ============ activation producer (whole warp, elected issue) ===========
+        pdl_wait();  // x is the previous kernel's output
         uint32_t it = 0;
         while (iter.next(a, sg)) {
             const int mt = sg.tile / a.NT;
@@ -488,6 +494,7 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads, 1)
         }
     } else if (warp >= C::kEpiWarp0) {
         // ===================== epilogue =====================
+        pdl_wait();  // y / residual / workspace are shared with the previous kernel
         const int lq = warp & 3;
         const int r = lq * 32 + lane;
         const uint32_t lane_addr = static_cast<uint32_t>(lq * 32) << 16;
@@ -625,8 +632,17 @@ cudaError_t launch_one(const CUtensorMap& map, const qgemm_args& a, int grid,
         if (e != cudaSuccess) return e;
         attr_done = true;
     }
-    qgemm_kernel<BITS, SYM, BN, SPS><<<grid, C::kThreads, C::kSmem, st>>>(map, a);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(C::kThreads);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, qgemm_kernel<BITS, SYM, BN, SPS>, map, a);
 }
 
 template <int BN>

@@ -68,6 +68,15 @@ __device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
     } while (!__all_sync(0xffffffffu, done));
 }
 
+// ---- programmatic dependent launch ------------------------------------------
+// wait: block until the preceding grid in the stream completed and its memory
+// is visible; trigger: let the next grid start launching (its prologue and
+// weight streaming overlap this grid's tail).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---- async copies ---------------------------------------------------------
 // 1-D bulk copy global -> shared, completes tx bytes on `bar`.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src,
