@@ -65,7 +65,7 @@ __device__ __forceinline__ void trace_ev(const qgemm_args& a, int role, uint32_t
 #ifndef HP_QGEMM_TRACE
     return;  // production build: tracing compiled out
 #endif
-    if (role < 4 && a.trace && blockIdx.x == g_trace_cta && it < kTraceIters) {
+    if (role < 6 && a.trace && blockIdx.x == g_trace_cta && it < kTraceIters) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         a.trace[(role * kTraceIters + it) * 4 + ev] = t;
@@ -142,8 +142,12 @@ struct seg_iter {
 template <int BITS, int BN, int SPS>
 struct qgemm_cfg {
     // Dequant warpgroups: decode 3/4/8-bit use 3 warpgroups taking whole
-    // stages round-robin (latency hiding for the ALU/FMA-bound dequant);
-    // prefill and 16-bit decode use 2 warpgroups splitting every stage.
+    // stages round-robin (amortises the per-stage barrier work over 8
+    // slices per warp); prefill and 16-bit decode use 2 warpgroups splitting
+    // every stage. One CTA per SM (all 512 TMEM columns).
+    static constexpr bool kCoRes = false;
+    static constexpr int kMinBlocks = 1;
+    static constexpr int kTmemCols = 512;
     static constexpr bool kRR = BN <= 64 && BITS != 16;
     static constexpr int DWG = kRR ? 3 : 2;
     static constexpr int kThreads = 128 * (2 + DWG);
@@ -168,7 +172,7 @@ struct qgemm_cfg {
     static constexpr int A0_ = NACC * BN < 64 ? 64 : NACC * BN;
     static constexpr int A0 = (A0_ + 63) / 64 * 64;
     static constexpr int ACOLS = 16 * SPS;                       // TMEM columns per A stage
-    static constexpr int AS_ = (512 - A0) / ACOLS > 8 ? 8 : (512 - A0) / ACOLS;
+    static constexpr int AS_ = (kTmemCols - A0) / ACOLS > 8 ? 8 : (kTmemCols - A0) / ACOLS;
     static constexpr int AS = kRR ? (AS_ / DWG) * DWG : AS_;
     static constexpr int kCodesOff = BR * kB;                    // B ring first (1024-aligned)
     static constexpr int kStgOff = kCodesOff + CR * kCS;         // epilogue staging [16][kStgLd] fp32
@@ -180,7 +184,7 @@ struct qgemm_cfg {
     static_assert(AS >= 2, "need >= 2 TMEM A stages");
     static_assert(!kRR || (CR % DWG == 0 && AS % DWG == 0), "round-robin ring depth");
     static_assert(SPS == 2 || SPS == 4 || SPS == 8, "SPS");
-    static_assert(kSmem <= 227 * 1024, "smem");
+    static_assert(kSmem <= (kCoRes ? 113 : 227) * 1024, "smem");
 };
 
 // Epilogue write-out of 16 tokens x 128 rows through shared memory: each
@@ -250,7 +254,8 @@ __device__ __forceinline__ void stage_store16(const qgemm_args& a, float* stg, i
 }
 
 template <int BITS, bool SYM, int BN, int SPS>
-__global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads, 1)
+__global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
+                                  qgemm_cfg<BITS, BN, SPS>::kMinBlocks)
     qgemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const qgemm_args a) {
     using C = qgemm_cfg<BITS, BN, SPS>;
     constexpr int AS = C::AS, NACC = C::NACC;
@@ -286,7 +291,7 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads, 1)
     if (threadIdx.x == 0 && a.trace) {  // per-CTA entry time
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        a.trace[4 * kTraceIters * 4 + 2 * blockIdx.x] = t;
+        a.trace[6 * kTraceIters * 4 + 2 * blockIdx.x] = t;
         clk0 = clock64();
     }
 #endif
@@ -311,7 +316,7 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads, 1)
         fence_mbar_init();
     }
     if (warp == 3 && lane == 0) prefetch_tmap(&tmap_x);
-    if (warp == 2) tmem_alloc<512>(tmem_slot);
+    if (warp == 2) tmem_alloc<C::kTmemCols>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -474,6 +479,7 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads, 1)
                 // ... then hand the weight slot back to the producer at once
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty_c[s]);
+                if (trole >= 0) trace_ev(a, 4, it, 0);
                 // phase 2: convert + store into the TMEM A stage
 #pragma unroll
                 for (int h = 0; h < kSl; ++h) {
@@ -485,7 +491,9 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads, 1)
                         tmem_st16(tmem + lane_addr + C::A0 + as * C::ACOLS + (x0 + h) * 16, v);
                     }
                 }
+                if (trole >= 0) trace_ev(a, 4, it, 1);
                 tmem_st_wait();
+                if (trole >= 0) trace_ev(a, 4, it, 2);
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&afull[as]);
@@ -540,29 +548,27 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads, 1)
                 asm volatile("bar.sync 1, 128;" ::: "memory");
                 if (*bcast == static_cast<unsigned>(sg.nseg - 1)) {
                     __threadfence();
-                    // ordered reduction of all segments of this tile (row r)
+                    // ordered reduction of all segments of this tile (row r), 16
+                    // tokens at a time (keeps the epilogue within 64 registers)
                     const float* base = a.partial + (static_cast<size_t>(sg.tile) * a.maxseg * 128 + r) * BN;
-                    float accv[BN];
-#pragma unroll
-                    for (int i = 0; i < BN; ++i) accv[i] = 0.f;
-                    for (int j = 0; j < sg.nseg; ++j) {
-                        const float4* src = reinterpret_cast<const float4*>(base + static_cast<size_t>(j) * 128 * BN);
-                        float4 tmp[BN / 4];
-#pragma unroll
-                        for (int i = 0; i < BN / 4; ++i) tmp[i] = __ldcg(src + i);
-#pragma unroll
-                        for (int i = 0; i < BN / 4; ++i) {
-                            accv[4 * i] += tmp[i].x;
-                            accv[4 * i + 1] += tmp[i].y;
-                            accv[4 * i + 2] += tmp[i].z;
-                            accv[4 * i + 3] += tmp[i].w;
-                        }
-                    }
-#pragma unroll
+#pragma unroll 1
                     for (int c0 = 0; c0 < BN; c0 += 16) {
                         float f[16];
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) f[i] = accv[c0 + i];
+                        for (int i = 0; i < 16; ++i) f[i] = 0.f;
+#pragma unroll 1
+                        for (int j = 0; j < sg.nseg; ++j) {
+                            const float4* src = reinterpret_cast<const float4*>(
+                                base + static_cast<size_t>(j) * 128 * BN + c0);
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                const float4 q4 = __ldcg(src + i);
+                                f[4 * i] += q4.x;
+                                f[4 * i + 1] += q4.y;
+                                f[4 * i + 2] += q4.z;
+                                f[4 * i + 3] += q4.w;
+                            }
+                        }
                         stage_store16(a, stg, C::kStgLd, r, f, mt * BN + c0, nt * 128);
                     }
                     if (warp == C::kEpiWarp0 && lane == 0) a.counters[sg.tile] = 0u;
@@ -579,17 +585,17 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads, 1)
     if (threadIdx.x == 0 && a.trace) {  // per-CTA exit time
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        a.trace[4 * kTraceIters * 4 + 2 * blockIdx.x + 1] = t;
-        a.trace[4 * kTraceIters * 4 + 2048 + blockIdx.x] = static_cast<unsigned long long>(clock64() - clk0);
+        a.trace[6 * kTraceIters * 4 + 2 * blockIdx.x + 1] = t;
+        a.trace[6 * kTraceIters * 4 + 2048 + blockIdx.x] = static_cast<unsigned long long>(clock64() - clk0);
         unsigned smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        a.trace[4 * kTraceIters * 4 + 3072 + blockIdx.x] = smid;
+        a.trace[6 * kTraceIters * 4 + 3072 + blockIdx.x] = smid;
     }
 #endif
     (void)clk0;
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc<512>(tmem);
+        tmem_dealloc<C::kTmemCols>(tmem);
     }
 }
 
@@ -708,8 +714,8 @@ unsigned long long* trace_buffer() {
         if (getenv("HP_QGEMM_TRACE")) {
             int cta = getenv("HP_QGEMM_TRACE_CTA") ? atoi(getenv("HP_QGEMM_TRACE_CTA")) : 0;
             cudaMemcpyToSymbol(g_trace_cta, &cta, sizeof(int));
-            cudaMalloc(&g_trace, sizeof(unsigned long long) * (4 * kTraceIters * 4 + 4 * 1024));
-            cudaMemset(g_trace, 0, sizeof(unsigned long long) * (4 * kTraceIters * 4 + 4 * 1024));
+            cudaMalloc(&g_trace, sizeof(unsigned long long) * (6 * kTraceIters * 4 + 4 * 1024));
+            cudaMemset(g_trace, 0, sizeof(unsigned long long) * (6 * kTraceIters * 4 + 4 * 1024));
         }
     }
     return g_trace;

@@ -22,10 +22,10 @@ def main():
     for _ in range(3):
         qweight.qlinear(qw, x, phase=1)
     torch.cuda.synchronize()
-    buf = np.zeros(4 * 64 * 4 + 4 * 1024, dtype=np.uint64)
+    buf = np.zeros(6 * 64 * 4 + 4 * 1024, dtype=np.uint64)
     lib.hp_debug_trace(buf.ctypes.data, buf.size)
-    cyc = buf[4 * 64 * 4 + 2048:4 * 64 * 4 + 2048 + 148].astype(np.int64)
-    cta = buf[4 * 64 * 4:4 * 64 * 4 + 2048].reshape(1024, 2).astype(np.int64)
+    cyc = buf[6 * 64 * 4 + 2048:6 * 64 * 4 + 2048 + 148].astype(np.int64)
+    cta = buf[6 * 64 * 4:6 * 64 * 4 + 2048].reshape(1024, 2).astype(np.int64)
     cta = cta[cta[:, 0] > 0]
     t0c = cta[:, 0].min()
     ent = (cta[:, 0] - t0c) / 1000
@@ -34,7 +34,7 @@ def main():
           f"exit min/med/max {ext.min():.2f}/{np.median(ext):.2f}/{ext.max():.2f} us")
     print("  exit sorted (last 10):", np.round(np.sort(ext)[-10:], 2), " argmax", int(np.argmax(ext)))
     print("  exit by CTA:", " ".join(f"{v:.1f}" for v in ext))
-    smid = buf[4 * 64 * 4 + 2048 + 1024:4 * 64 * 4 + 2048 + 1024 + 148].astype(np.int64)
+    smid = buf[6 * 64 * 4 + 2048 + 1024:6 * 64 * 4 + 2048 + 1024 + 148].astype(np.int64)
     print("  smid by CTA:", " ".join(str(v) for v in smid))
     span_ns = (cta[:148, 1] - cta[:148, 0]).astype(np.float64)
     print(f"  CTA cycles/ns (implied GHz): median {np.median(cyc / span_ns):.3f}, cycles median {np.median(cyc):.0f}")
@@ -50,11 +50,12 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(); g.replay(); e1.record(); torch.cuda.synchronize()
     print(f"  graph b2b per launch: {e0.elapsed_time(e1) * 100:.1f} us")
-    t = buf[:4 * 64 * 4].reshape(4, 64, 4).astype(np.int64)
+    t = buf[:6 * 64 * 4].reshape(6, 64, 4).astype(np.int64)
     t0 = t[t > 0].min()
     names = ["producer (start, empty_ok, issued)", "mma (start, full_ok, afull_ok, committed)",
-             "dequant w4 (start, full_ok, aempty_ok, arrived)", "epilogue seg (start, tfull_ok, stored, fixup_done) @48.., kernel entry/exit @63"]
-    for r in range(4):
+             "dequant w4 (start, full_ok, aempty_ok, arrived)", "epilogue seg (start, tfull_ok, stored, fixup_done) @48..",
+             "dequant w4 detail (codes_loaded, st_issued, st_done, -)", "unused"]
+    for r in range(5):
         print(names[r])
         for it in range(0, 64):
             row = t[r, it]
