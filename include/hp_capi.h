@@ -199,6 +199,10 @@ hp_status hp_host_simulate(const double* costs4, int n_stages, int B, int eta,
                            int xi, int n, double* out4, double* busy,
                            double* timeline, int64_t timeline_cap);
 hp_status hp_host_plan_check(const char* plan_json, char* out, int64_t cap);
+/* Unit execution order of one stage: (kind 0 prefill / 1 decode, index,
+ * token) triples into out3[3*cap]; *n = count.                          */
+hp_status hp_host_unit_order(const char* plan_json, const char* model_json, int stage,
+                             int* out3, int cap, int* n);
 
 #ifdef __cplusplus
 }

@@ -209,6 +209,36 @@ hp_status hp_host_plan_check(const char* plan_json, char* out, int64_t cap) {
     }
 }
 
+// Static unit order of stage `stage` (kind, index, token triples) for the
+// plan — what the executor runs, and what the multi-process tests check.
+hp_status hp_host_unit_order(const char* plan_json, const char* model_json, int stage,
+                             int* out3, int cap, int* n) {
+    try {
+        const auto doc = hetplan::plan_io::parse_plan(plan_json);
+        nlohmann::ordered_json cfg;
+        cfg["model"] = nlohmann::ordered_json::parse(model_json);
+        cfg["cluster"]["devices"] = nlohmann::ordered_json::array(
+            {{{"name", "b200"}, {"mem_bytes", 1}, {"link_bw_bytes_per_s", 9e11}}});
+        cfg["workload"] = {{"B", doc.load.global_bz}, {"s", doc.load.prompt_len}, {"n", doc.load.gen_len}};
+        cfg["bits"] = doc.bits;
+        const auto rs = hetplan::parse_config(cfg.dump());
+        const auto order = hetplan::runtime::static_unit_order(doc, rs.model);
+        if (stage < 0 || stage >= static_cast<int>(order.size()))
+            throw std::invalid_argument("unit_order: bad stage");
+        const auto& u = order[stage];
+        if (static_cast<int>(u.size()) > cap) throw std::invalid_argument("unit_order: capacity");
+        for (size_t i = 0; i < u.size(); ++i) {
+            out3[3 * i] = u[i].kind == hetplan::pipesim::unit_kind::prefill ? 0 : 1;
+            out3[3 * i + 1] = u[i].index;
+            out3[3 * i + 2] = u[i].token;
+        }
+        *n = static_cast<int>(u.size());
+        return HP_OK;
+    } catch (const std::exception& e) {
+        return from_exception(e);
+    }
+}
+
 struct hp_pipeline {
     std::unique_ptr<hetplan::runtime::pipeline> impl;
     int64_t units = 0, layers = 0;

@@ -118,6 +118,7 @@ def run(name: str) -> str:
     (OUT / f"{name}.json").write_text(json.dumps(doc, indent=1))
     (OUT / f"{name}.omega.csv").write_text(omega)
     (OUT / f"{name}.config.json").write_text(json.dumps(cfg, indent=1))
+    (OUT / f"{name}.latency.json").write_text(latency_json(c["model"]))
     return f"{name}: {dt:.0f}s bits={doc['layer_bits']} stages={[s['layers'] for s in doc['stages']]} eta={doc['eta']} xi={doc['xi']} optimal={doc['optimal']}"
 
 

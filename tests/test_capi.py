@@ -1,0 +1,77 @@
+"""The C-ABI boundary: every function declared in include/hp_capi.h is
+exported by libhetplan_b200.so, and without a B200 the compute entry points
+fail loudly (HP_ECUDA) instead of falling back to the CPU. CPU only."""
+import re
+from pathlib import Path
+
+import pytest
+
+from paper_2403_01136_b200 import capi
+
+HEADER = Path(__file__).resolve().parents[1] / "include" / "hp_capi.h"
+
+
+def declared_functions():
+    text = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+    names = re.findall(r"\b(hp_[a-z0-9_]+)\s*\(", text)
+    return sorted(set(names))
+
+
+def test_every_declared_symbol_is_exported():
+    names = declared_functions()
+    assert len(names) >= 25
+    missing = [n for n in names if not hasattr(capi.lib, n)]
+    assert not missing, missing
+    assert set(capi.EXPORTED) <= set(names)
+
+
+def test_abi_version_and_sizes():
+    assert capi.lib.hp_abi_version() == 1
+    # packed-size contract (memcost.cpp:15-18): ceil(n*k*b/8) on aligned shapes
+    for bits in (3, 4, 8, 16):
+        assert capi.lib.hp_packed_bytes(5120, 20480, bits) == 5120 * 20480 * bits // 8
+    assert capi.lib.hp_packed_bytes(0, 10, 4) == -1
+    assert capi.lib.hp_packed_bytes(10, 10, 5) == -1
+    assert capi.lib.hp_scale_count(256, 300) == 2 * 3 * 128
+
+
+@pytest.mark.skipif(capi.device_ok(), reason="a B200 is present")
+def test_no_cpu_fallback_without_device():
+    import ctypes as C
+    st = capi.lib.hp_quant_pack(C.c_void_p(16), 128, 128, 128, 4, 1, 0, C.c_void_p(16),
+                                C.c_void_p(16), None, None, None, None)
+    assert st == capi.HP_ECUDA
+    assert b"no usable sm_100" in capi.lib.hp_last_error()
+    w = capi.hp_qweight(128, 128, 4, 1, 16, 16, None)
+    st = capi.lib.hp_qlinear(C.byref(w), C.c_void_p(16), 128, 8, C.c_void_p(16), 128, None, 0,
+                             0, capi.HP_DECODE, None, 0, None)
+    assert st == capi.HP_ECUDA
+
+
+def test_invalid_arguments_are_einval():
+    import ctypes as C
+    st = capi.lib.hp_quant_pack(None, 128, 128, 128, 4, 1, 0, None, None, None, None, None, None)
+    assert st == capi.HP_EINVAL
+    st = capi.lib.hp_quant_pack(C.c_void_p(16), 128, 128, 128, 5, 1, 0, C.c_void_p(16),
+                                C.c_void_p(16), None, None, None, None)
+    assert st == capi.HP_EINVAL
+    st = capi.lib.hp_quant_pack(C.c_void_p(16), 128, 128, 128, 4, 1, capi.HP_STOCHASTIC,
+                                C.c_void_p(16), C.c_void_p(16), None, None, None, None)
+    assert st == capi.HP_EINVAL and b"round-to-nearest" in capi.lib.hp_last_error()
+
+
+def test_plan_documents_round_trip_and_validate():
+    import ctypes as C
+    import json
+    plans = Path(__file__).resolve().parent / "golden" / "plans"
+    for f in sorted(plans.glob("*gpu.json")):
+        buf = C.create_string_buffer(1 << 20)
+        capi.check(capi.lib.hp_host_plan_check(f.read_bytes(), buf, len(buf)))
+        a, b = json.loads(f.read_text()), json.loads(buf.value)
+        for k in ("layer_bits", "eta", "xi", "device_order", "objective"):
+            assert a[k] == b[k], (f.name, k)
+        assert [s["layers"] for s in a["stages"]] == [s["layers"] for s in b["stages"]]
+    bad = json.loads((plans / "opt13b_b32_1gpu.json").read_text())
+    bad["layer_bits"][0] = 5
+    with pytest.raises(capi.InvalidArgument):
+        capi.check(capi.lib.hp_host_plan_check(json.dumps(bad).encode(), buf, len(buf)))
