@@ -23,6 +23,7 @@
 #include <array>
 #include <cstdint>
 #include <memory>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
@@ -39,6 +40,15 @@ struct pipeline_options {
     bool use_graphs = true;     // capture each unit's stage forward
     bool instrument = false;    // CUDA events around every linear op
     int sm_budget = 0;          // persistent-kernel grid cap (0 = all SMs)
+    double timeout_s = 0.0;     // run() watchdog (0 = wait forever); on
+                                // expiry throws pipeline_timeout with the
+                                // per-stream progress of the stuck round
+};
+
+// run() exceeded pipeline_options::timeout_s (hp_pipeline_run -> HP_ETIMEOUT).
+// The stuck round still occupies the device; destroy the pipeline.
+struct pipeline_timeout : std::runtime_error {
+    using std::runtime_error::runtime_error;
 };
 
 struct run_timing {

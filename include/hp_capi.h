@@ -155,6 +155,9 @@ typedef struct {
     int32_t sm_budget;   /* persistent-kernel grid cap, 0 = all SMs         */
     uint64_t seed;       /* synthetic tensors (oracle/synth.py mirror)     */
     double weight_std;   /* synthetic weight std (0.02)                    */
+    double timeout_s;    /* hp_pipeline_run watchdog, 0 = none; expiry ->
+                          * HP_ETIMEOUT with per-stream progress in
+                          * hp_last_error (destroy the pipeline after)     */
 } hp_pipeline_options;
 hp_status hp_nccl_unique_id(void* out128);
 hp_status hp_pipeline_create(const char* plan_json, const char* model_json, int rank,

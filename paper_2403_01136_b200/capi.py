@@ -56,6 +56,7 @@ class hp_pipeline_options(C.Structure):
         ("sm_budget", C.c_int32),
         ("seed", C.c_uint64),
         ("weight_std", C.c_double),
+        ("timeout_s", C.c_double),
     ]
 
 

@@ -28,6 +28,7 @@ hp_status from_exception(const std::exception& e) {
     hp_detail::set_error(e.what());
     if (dynamic_cast<const hetplan::infeasible_error*>(&e)) return HP_EINFEASIBLE;
     if (dynamic_cast<const std::invalid_argument*>(&e)) return HP_EINVAL;
+    if (dynamic_cast<const hetplan::runtime::pipeline_timeout*>(&e)) return HP_ETIMEOUT;
     return HP_EINTERNAL;
 }
 
@@ -281,6 +282,7 @@ hp_status hp_pipeline_create(const char* plan_json, const char* model_json, int 
             po.sm_budget = opt->sm_budget;
             po.seed = opt->seed;
             po.weight_std = opt->weight_std > 0 ? opt->weight_std : 0.02;
+            po.timeout_s = opt->timeout_s;
         }
         std::vector<std::array<char, 128>> ids;
         if (world > 1) {

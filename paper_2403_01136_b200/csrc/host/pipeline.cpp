@@ -18,6 +18,10 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <thread>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -56,6 +60,24 @@ void hp_ok(hp_status s, const char* what) {
 
 // Timing events inside a captured round must stay real event records (an
 // internal graph event node cannot be timed): record them as "external".
+// HP_PIPE_DEBUG=1: trace every host-side NCCL / sync call to stderr.
+bool pipe_debug() {
+    static const bool on = [] {
+        const char* e = std::getenv("HP_PIPE_DEBUG");
+        return e && *e && *e != '0';
+    }();
+    return on;
+}
+#define PDBG(...)                                             \
+    do {                                                      \
+        if (pipe_debug()) {                                   \
+            std::fprintf(stderr, "[hp pipe r%d] ", rank);     \
+            std::fprintf(stderr, __VA_ARGS__);                \
+            std::fputc('\n', stderr);                        \
+            std::fflush(stderr);                              \
+        }                                                     \
+    } while (0)
+
 cudaError_t timing_record(cudaEvent_t e, cudaStream_t st) {
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     cudaError_t r = cudaStreamIsCapturing(st, &cap);
@@ -168,6 +190,8 @@ struct pipeline::impl {
     std::vector<cudaEvent_t> unit_ev;        // 2 per unit
     std::vector<cudaEvent_t> recv_ev;        // per incoming message
     std::vector<cudaEvent_t> comp_ev;        // per outgoing message
+    size_t comp_used = 0;
+    bool timed_out = false;
     std::vector<cudaEvent_t> op_ev[2];       // instrumented unit per phase
     int instr_unit[2] = {-1, -1};
     kernel_stats kstats[2];
@@ -293,6 +317,9 @@ struct pipeline::impl {
             cuda_ok(cudaMemsetAsync(ws, 0, ws_bytes, cs), "ws");
         }
 
+        load_kernels();
+        if (world > 1) connect_links();
+
         // ---- events ------------------------------------------------------
         cuda_ok(cudaEventCreate(&ev_t0), "ev");
         cuda_ok(cudaEventCreate(&ev_t1), "ev");
@@ -366,6 +393,79 @@ struct pipeline::impl {
         }
     }
 
+    // CUDA loads a kernel's module lazily at its first launch, and that load
+    // waits for the device: issued while an NCCL recv kernel spins on rs (it
+    // waits for a message this very stage must first compute and send) it
+    // never returns. So run every (phase, rows) forward the round will use,
+    // plus the gather, once on scratch before any NCCL operation is posted.
+    void load_kernels() {
+        std::vector<std::pair<int64_t, int>> shapes;
+        for (int k = 0; k < static_cast<int>(sched.prefill_sizes.size()); ++k)
+            shapes.push_back({prefill_rows(k), HP_PREFILL});
+        for (int g = 0; g < sched.num_groups; ++g) shapes.push_back({group_size[g], HP_DECODE});
+        std::sort(shapes.begin(), shapes.end());
+        shapes.erase(std::unique(shapes.begin(), shapes.end()), shapes.end());
+        int64_t rows = 1;
+        for (const auto& sh : shapes) rows = std::max(rows, sh.first);
+        void* x = nullptr;
+        cuda_ok(cudaMalloc(&x, static_cast<size_t>(rows) * h1 * 2 * 2), "cudaMalloc scratch");
+        cuda_ok(hp::launch_synth(x, rows * h1, seed_for({5}), 0.0, 1.0, cs), "synth scratch");
+        for (const auto& sh : shapes) forward(x, sh.first, sh.second, false);
+        cuda_ok(hp::launch_gather_rows(x, h1, 1, 0, 1, static_cast<int>(h1),
+                                       static_cast<char*>(x) + static_cast<size_t>(rows) * h1 * 2, h1,
+                                       cs),
+                "gather");
+        cuda_ok(cudaStreamSynchronize(cs), "load kernels");
+        cuda_ok(cudaFree(x), "cudaFree scratch");
+        if (ws_bytes) cuda_ok(cudaMemsetAsync(ws, 0, ws_bytes, cs), "ws");
+    }
+
+    // NCCL connects P2P channels lazily, host-blocking, on the first
+    // send/recv that needs them (how many channels / which protocol depends
+    // on the message size) and needs the peer to connect the SAME link
+    // concurrently. A round posts rank 0's feedback recvs (link world-1)
+    // first while rank 1 waits on link 0 -> a cycle of blocked hosts. So
+    // exchange one message of every size the round uses on each link here,
+    // in ascending link order (rank r: link r-1 then link r; rank 0: link 0
+    // then link world-1) -- a chain, which cannot deadlock.
+    std::vector<size_t> link_counts(int l) const {
+        std::vector<size_t> c;
+        if (l < world - 1) {
+            for (int k = 0; k < static_cast<int>(sched.prefill_sizes.size()); ++k)
+                c.push_back(static_cast<size_t>(prefill_rows(k)) * h1);
+        }
+        for (int g = 0; g < sched.num_groups; ++g) c.push_back(static_cast<size_t>(group_size[g]) * h1);
+        std::sort(c.begin(), c.end());
+        c.erase(std::unique(c.begin(), c.end()), c.end());
+        return c;
+    }
+    void connect_links() {
+        const int prev = (rank - 1 + world) % world;
+        size_t maxc = 0;
+        for (int l : {rank, prev})
+            for (size_t c : link_counts(l)) maxc = std::max(maxc, c);
+        void* probe = nullptr;
+        cuda_ok(cudaMalloc(&probe, maxc * 2), "cudaMalloc probe");
+        auto link = [&](bool out) {
+            for (size_t c : link_counts(out ? rank : prev)) {
+                PDBG("connect %s count %zu", out ? "out" : "in", c);
+                if (out)
+                    nccl_ok(ncclSend(probe, c, ncclBfloat16, /*peer=*/1, c_out, cs), "connect send");
+                else
+                    nccl_ok(ncclRecv(probe, c, ncclBfloat16, /*peer=*/0, c_in, cs), "connect recv");
+                cuda_ok(cudaStreamSynchronize(cs), "connect");
+            }
+        };
+        if (rank == 0) {
+            link(true);
+            link(false);
+        } else {
+            link(false);
+            link(true);
+        }
+        cuda_ok(cudaFree(probe), "cudaFree probe");
+    }
+
     // Enqueue one whole round on (cs, ss, rs). Capturable.
     void enqueue_round() {
         // fork side streams off the compute stream (joins them into a capture)
@@ -387,6 +487,7 @@ struct pipeline::impl {
                     dst = dec_x[u.index];
                     count = static_cast<size_t>(group_size[u.index]) * h1;
                 }
+                PDBG("recv %zu (kind %d idx %d tok %d) count %zu", i, static_cast<int>(u.kind), u.index, u.token, count);
                 nccl_ok(ncclRecv(dst, count, ncclBfloat16, /*peer=*/0, c_in, rs), "recv");
                 cuda_ok(cudaEventRecord(recv_ev[i], rs), "ev");
             }
@@ -407,6 +508,7 @@ struct pipeline::impl {
         for (size_t ui = 0; ui < units.size(); ++ui) {
             const unit_ref& u = units[ui];
             const bool pre = u.kind == pipesim::unit_kind::prefill;
+            PDBG("unit %zu (kind %d idx %d tok %d)", ui, static_cast<int>(u.kind), u.index, u.token);
             // ---- input dependency
             const bool needs_recv = world > 1 && (rank > 0 || !pre);
             if (needs_recv) {
@@ -425,8 +527,10 @@ struct pipeline::impl {
             if (!last) {
                 cuda_ok(cudaEventRecord(comp_ev[comp_i], cs), "ev");
                 cuda_ok(cudaStreamWaitEvent(ss, comp_ev[comp_i++], 0), "wait");
+                PDBG("send unit %zu count %zu", ui, static_cast<size_t>(m) * h1);
                 nccl_ok(ncclSend(x, static_cast<size_t>(m) * h1, ncclBfloat16, /*peer=*/1, c_out, ss),
                         "send");
+                PDBG("send unit %zu posted", ui);
                 continue;
             }
             if (pre) {
@@ -456,6 +560,7 @@ struct pipeline::impl {
                 if (--left[g] == 0 && n >= 2 && world > 1) {
                     cuda_ok(cudaEventRecord(comp_ev[comp_i], cs), "ev");
                     cuda_ok(cudaStreamWaitEvent(ss, comp_ev[comp_i++], 0), "wait");
+                    PDBG("send fb group %d count %zu", g, static_cast<size_t>(group_size[g]) * h1);
                     nccl_ok(ncclSend(fb[g], static_cast<size_t>(group_size[g]) * h1, ncclBfloat16,
                                      /*peer=*/1, c_out, ss),
                             "send fb");
@@ -463,15 +568,55 @@ struct pipeline::impl {
             } else if (world > 1 && u.token + 1 <= n - 1) {
                 cuda_ok(cudaEventRecord(comp_ev[comp_i], cs), "ev");
                 cuda_ok(cudaStreamWaitEvent(ss, comp_ev[comp_i++], 0), "wait");
+                PDBG("send fb unit %zu count %zu", ui, static_cast<size_t>(m) * h1);
                 nccl_ok(ncclSend(x, static_cast<size_t>(m) * h1, ncclBfloat16, /*peer=*/1, c_out, ss),
                         "send fb");
             }
         }
+        comp_used = static_cast<size_t>(comp_i);
         // join side streams back into the compute stream
         cuda_ok(cudaEventRecord(ev_join_s, ss), "ev");
         cuda_ok(cudaStreamWaitEvent(cs, ev_join_s, 0), "wait");
         cuda_ok(cudaEventRecord(ev_join_r, rs), "ev");
         cuda_ok(cudaStreamWaitEvent(cs, ev_join_r, 0), "wait");
+    }
+
+    // Block until cs drains; with opt.timeout_s > 0 poll instead and, on
+    // expiry, throw pipeline_timeout naming how far each stream got.
+    void wait_round(const char* what) {
+        PDBG("wait %s", what);
+        if (opt.timeout_s <= 0) {
+            cuda_ok(cudaStreamSynchronize(cs), what);
+            return;
+        }
+        const auto t0 = std::chrono::steady_clock::now();
+        for (;;) {
+            const cudaError_t e = cudaStreamQuery(cs);
+            if (e == cudaSuccess) return;
+            if (e != cudaErrorNotReady) cuda_ok(e, what);
+            const double dt =
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            if (dt > opt.timeout_s) break;
+            std::this_thread::sleep_for(std::chrono::microseconds(dt < 0.01 ? 20 : 2000));
+        }
+        auto done = [](cudaEvent_t ev) { return cudaEventQuery(ev) == cudaSuccess; };
+        size_t u_done = 0, r_done = 0, c_done = 0;
+        while (u_done < units.size() && done(unit_ev[2 * u_done + 1])) ++u_done;
+        while (r_done < recv_ev.size() && done(recv_ev[r_done])) ++r_done;
+        while (c_done < comp_used && done(comp_ev[c_done])) ++c_done;
+        std::string msg = std::string("pipeline: ") + what + " exceeded " +
+                          std::to_string(opt.timeout_s) + " s on rank " + std::to_string(rank) +
+                          ": units done " + std::to_string(u_done) + "/" +
+                          std::to_string(units.size()) + ", recvs done " + std::to_string(r_done) +
+                          "/" + std::to_string(recv_ev.size()) + ", sends ready " +
+                          std::to_string(c_done) + "/" + std::to_string(comp_used);
+        if (u_done < units.size()) {
+            const unit_ref& u = units[u_done];
+            msg += ", stuck at unit (" + std::string(u.kind == pipesim::unit_kind::prefill ? "prefill" : "decode") +
+                   " " + std::to_string(u.index) + " token " + std::to_string(u.token) + ")";
+        }
+        timed_out = true;
+        throw pipeline_timeout(msg);
     }
 
     void capture() {
@@ -497,7 +642,7 @@ struct pipeline::impl {
         if (opt.use_graphs) {
             if (!graph_ready) {
                 enqueue_round();  // eager warm-up (sets kernel attributes)
-                cuda_ok(cudaStreamSynchronize(cs), "warmup");
+                wait_round("warm-up round");
                 if (rank == 0) {
                     const size_t bytes = static_cast<size_t>(B) * s * h1 * 2;
                     cuda_ok(cudaMemcpyAsync(prompt, host_prompt ? host_prompt : pristine, bytes,
@@ -523,7 +668,7 @@ struct pipeline::impl {
             }
         }
         cuda_ok(cudaEventRecord(ev_t1, cs), "ev");
-        cuda_ok(cudaStreamSynchronize(cs), "round");
+        wait_round("round");
         float ms = 0.f;
         cuda_ok(cudaEventElapsedTime(&ms, ev_t0, ev_t1), "elapsed");
         t.makespan_s = ms * 1e-3;
@@ -562,8 +707,23 @@ struct pipeline::impl {
 
     ~impl() {
         if (graph) cudaGraphExecDestroy(graph);
-        if (c_in) ncclCommDestroy(c_in);
-        if (c_out) ncclCommDestroy(c_out);
+        // Destroy finalizes with the peer: same chain order as connect_links
+        // (rank 0: link 0 then link world-1; rank r: link r-1 then link r).
+        // After a timeout the round is still stuck on the device: abort.
+        auto close = [&](ncclComm_t c) {
+            if (!c) return;
+            if (timed_out)
+                ncclCommAbort(c);
+            else
+                ncclCommDestroy(c);
+        };
+        if (rank == 0) {
+            close(c_out);
+            close(c_in);
+        } else {
+            close(c_in);
+            close(c_out);
+        }
         auto f = [](void* p) {
             if (p) cudaFree(p);
         };
