@@ -232,6 +232,9 @@ def main():
     k0 = [pipe.kernel_stats(0), pipe.kernel_stats(1)]
     barrier()
     times, pre_s, dec_s = [], [], []
+    # cudaProfilerStart/Stop bracket the timed rounds so `ncu
+    # --profile-from-start off` lists exactly these launches (profiles/)
+    torch.cuda.profiler.start()
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             t = pipe.run()
@@ -239,6 +242,7 @@ def main():
             pre_s.append(t.prefill_s)
             dec_s.append(t.decode_s)
         barrier()
+    torch.cuda.profiler.stop()
     k1 = [pipe.kernel_stats(0), pipe.kernel_stats(1)]
     step_s = max_over_ranks(statistics.mean(times))
     pre_busy = max_over_ranks(statistics.mean(pre_s))
@@ -281,13 +285,21 @@ def main():
         k4 = d_pre["flops"] / d_pre["seconds"] / 1e12 if d_pre["seconds"] > 0 else None
         k3 = d_dec["bytes"] / d_dec["seconds"] / 1e9 if d_dec["seconds"] > 0 else None
         prof = ROOT / "profiles" / "ncu_traffic.json"
-        traffic = None
-        if prof.exists():
-            traffic = json.loads(prof.read_text()).get(name, {}).get("k4_traffic_bytes")
+        ncu = json.loads(prof.read_text()).get(name, {}) if prof.exists() else {}
+
+        def traffic(k):  # DRAM bytes per launch from the committed ncu --set full capture
+            e = ncu.get(k)
+            return e["dram_bytes_per_launch"] if e else None
+
+        def traffic_note(k):
+            e = ncu.get(k)
+            return ({"captured_launches": e["launches"], "alg_bytes_per_launch": e["alg_bytes_per_launch"],
+                     "source": e["source"]} if e else None)
         pre_share = pre_busy / (pre_busy + dec_busy) if pre_busy + dec_busy > 0 else 0
         roof_pre = {"kernel": "K4 prefill dequant-GEMM (hp::qgemm_kernel, BN=256)",
                     "bound": "tensor", "achieved": k4, "peak": tf_sus, "unit": "TFLOP/s",
-                    "frac": k4 / tf_sus if k4 else None, "traffic": traffic,
+                    "frac": k4 / tf_sus if k4 else None, "traffic": traffic("k4"),
+                    "traffic_capture": traffic_note("k4"),
                     "peak_kind": f"{src} bf16_tflops_sustained (burst {tf_burst})",
                     "per_launch": {"launches": d_pre["launches"],
                                    "avg_flops": d_pre["flops"] / max(d_pre["launches"], 1),
@@ -296,7 +308,8 @@ def main():
         roof_dec = {"kernel": "K3 decode dequant-GEMV (hp::qgemm_kernel, BN=32, split-K)",
                     "bound": "hbm", "achieved": k3, "peak": hbm, "unit": "GB/s",
                     "frac": k3 / hbm if k3 else None, "frac_of_nominal_8TBs": k3 / 8000 if k3 else None,
-                    "traffic": None, "peak_kind": f"{src} hbm_gbs",
+                    "traffic": traffic("k3"), "traffic_capture": traffic_note("k3"),
+                    "peak_kind": f"{src} hbm_gbs",
                     "per_launch": {"launches": d_dec["launches"],
                                    "avg_bytes": d_dec["bytes"] / max(d_dec["launches"], 1),
                                    "avg_s": d_dec["seconds"] / max(d_dec["launches"], 1)},
