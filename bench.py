@@ -34,9 +34,22 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "decode tokens/s + prefill tok/s vs HBM/tensor roofline, 1/2/4/8 B200"
-PLAN_FOR_N = {1: "opt13b_b32_1gpu", 2: "opt30b_b32_2gpu", 4: "opt30b_b32_4gpu",
-              8: "opt66b_b32_8gpu"}
-CONFIG_INDEX = {1: 1, 2: 2, 4: 2, 8: 3}
+# The bench workload is configs[1] (OPT-13B, mixed 3/4/8/16-bit plan, B=32)
+# at every N: N>1 runs it weak-scaled as an N-stage pipeline -- B = 32 N
+# requests, xi = 32 (N decode groups in flight), same per-layer bits, stages
+# balanced on decode cost (tests/golden/make_plans.py weak). The other
+# BASELINE configs (OPT-30B/66B, BLOOM-176B plans) are parity-test cases,
+# runnable here with --plan.
+PLAN_FOR_N = {1: "opt13b_b32_1gpu", 2: "opt13b_b64_2gpu_weak", 4: "opt13b_b128_4gpu_weak",
+              8: "opt13b_b256_8gpu_weak"}
+CONFIG_INDEX = {1: 1, 2: 1, 4: 1, 8: 1}
+
+
+def workload_name(name: str, world: int) -> str:
+    if name == PLAN_FOR_N.get(world) and world > 1:
+        return (f"{name}: BASELINE.json configs[1] weak-scaled x{world} "
+                f"(B={32 * world}, {world}-stage pipeline)")
+    return f"{name} (BASELINE.json configs[{CONFIG_INDEX.get(world, 1)}])"
 
 
 def peaks():
@@ -160,8 +173,7 @@ def run_reference(args, rank: int, world: int):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{name} (BASELINE.json configs[{CONFIG_INDEX.get(world, 1)}])",
-                       "plan": name},
+            "config": {"workload": workload_name(name, world), "plan": name},
             "cpu_baseline": {"value": v, "unit": "tok/s", "cores": threads, "kind": "port",
                              "sample": vals[0]["sample"] +
                              "; the reference implements no layer forward (SPEC.md:8), so its "
@@ -343,7 +355,8 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "bf16 (weights 3/4/8/16-bit, fp32 accumulate)",
             "data": "synthetic (bit-reproducible weights/prompts, oracle/synth.py)",
-            "config": {"workload": f"{name} (BASELINE.json configs[{CONFIG_INDEX.get(world, 1)}])",
+            "stage_costs_s": [[c[0], c[1]] for c in gathered],
+            "config": {"workload": workload_name(name, world), "parallelism": f"pp{world}",
                        "plan": name, "B": B, "s": s, "n": n, "eta": plan["eta"],
                        "xi": plan["xi"], "layer_bits": plan["layer_bits"],
                        "stages": [st["layers"] for st in plan["stages"]],

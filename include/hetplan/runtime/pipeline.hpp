@@ -82,6 +82,11 @@ public:
     // Measured per-unit costs of the last run for pipesim::simulate.
     pipesim::stage_cost measured_cost() const;
     const kernel_stats& stats(int phase) const;  // 0 prefill (K4), 1 decode (K3)
+    // Per-layer seconds (LN + 4 linear ops) of this stage's layers in the
+    // instrumented unit of the last run with instrument=true: one prefill
+    // micro-batch (phase 0) / one decode group-token (phase 1). The profile
+    // behind cost-balanced stage partitions (tests/golden/make_plans.py).
+    const std::vector<double>& layer_costs(int phase) const;
     void reset_stats();
     std::int64_t weight_bytes() const;
     int num_kernel_launches_per_round() const;

@@ -176,6 +176,11 @@ hp_status hp_pipeline_stage_costs(hp_pipeline* p, double* out4);
 /* Instrumented linear-op totals for phase (HP_PREFILL / HP_DECODE):
  * {launches, seconds, algorithmic_bytes, flops} accumulated over rounds. */
 hp_status hp_pipeline_kernel_stats(hp_pipeline* p, int phase, double* out4);
+/* Per-layer seconds (LN + 4 linear ops) of this stage's layers in the
+ * instrumented unit of the last instrument=1 round: one prefill micro-batch
+ * (HP_PREFILL) or one decode group-token (HP_DECODE); *n = layer count.   */
+hp_status hp_pipeline_layer_costs(hp_pipeline* p, int phase, double* out, int64_t cap,
+                                  int64_t* n);
 /* {packed weight bytes, kernel launches per round, units, layers}        */
 hp_status hp_pipeline_info(hp_pipeline* p, int64_t* out4);
 void hp_pipeline_destroy(hp_pipeline* p);

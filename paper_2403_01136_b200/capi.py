@@ -99,6 +99,7 @@ def _load() -> C.CDLL:
         "hp_pipeline_run": (i32, [v, v, v, P(d)]),
         "hp_pipeline_stage_costs": (i32, [v, P(d)]),
         "hp_pipeline_kernel_stats": (i32, [v, i32, P(d)]),
+        "hp_pipeline_layer_costs": (i32, [v, i32, P(d), i64, P(i64)]),
         "hp_pipeline_info": (i32, [v, P(i64)]),
         "hp_pipeline_destroy": (None, [v]),
     })
@@ -123,7 +124,7 @@ EXPORTED = [
     "hp_host_indicator_csv", "hp_host_omega_from_stats", "hp_host_memcost", "hp_host_preset",
     "hp_host_make_schedule", "hp_host_simulate", "hp_host_plan_check", "hp_host_unit_order", "hp_set_sm_budget", "hp_set_pdl",
     "hp_nccl_unique_id", "hp_pipeline_create", "hp_pipeline_run", "hp_pipeline_stage_costs",
-    "hp_pipeline_kernel_stats", "hp_pipeline_info", "hp_pipeline_destroy",
+    "hp_pipeline_kernel_stats", "hp_pipeline_layer_costs", "hp_pipeline_info", "hp_pipeline_destroy",
 ]
 
 

@@ -2,6 +2,7 @@
 // "host planning helpers"): the drop-in hetplan:: functions exposed with
 // plain types so the parity tests can drive them next to the reference
 // build. Exceptions are mapped to hp_status like the rest of the ABI.
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -336,6 +337,19 @@ hp_status hp_pipeline_kernel_stats(hp_pipeline* p, int phase, double* out4) {
     out4[1] = k.seconds;
     out4[2] = k.bytes;
     out4[3] = k.flops;
+    return HP_OK;
+}
+
+hp_status hp_pipeline_layer_costs(hp_pipeline* p, int phase, double* out, int64_t cap,
+                                  int64_t* n) {
+    if (!p || !n || (cap > 0 && !out)) return HP_EINVAL;
+    const auto& v = p->impl->layer_costs(phase);
+    *n = static_cast<int64_t>(v.size());
+    if (cap < *n) {
+        hp_detail::set_error("layer_costs: need cap >= " + std::to_string(*n));
+        return HP_EINVAL;
+    }
+    std::copy(v.begin(), v.end(), out);
     return HP_OK;
 }
 

@@ -193,6 +193,8 @@ struct pipeline::impl {
     size_t comp_used = 0;
     bool timed_out = false;
     std::vector<cudaEvent_t> op_ev[2];       // instrumented unit per phase
+    std::vector<cudaEvent_t> lay_ev[2];      // whole layer (LN + 4 ops), same unit
+    std::vector<double> layer_s[2];          // last instrumented run, per layer
     int instr_unit[2] = {-1, -1};
     kernel_stats kstats[2];
     std::vector<double> unit_s;
@@ -343,6 +345,9 @@ struct pipeline::impl {
         for (int ph = 0; ph < 2; ++ph) {
             op_ev[ph].resize(static_cast<size_t>(layers.size()) * 4 * 2);
             for (auto& e : op_ev[ph]) cuda_ok(cudaEventCreate(&e), "ev");
+            lay_ev[ph].resize(static_cast<size_t>(layers.size()) * 2);
+            for (auto& e : lay_ev[ph]) cuda_ok(cudaEventCreate(&e), "ev");
+            layer_s[ph].assign(layers.size(), 0.0);
         }
         cuda_ok(cudaStreamSynchronize(cs), "init");
     }
@@ -378,6 +383,7 @@ struct pipeline::impl {
         for (size_t li = 0; li < layers.size(); ++li) {
             const layer& L = layers[li];
             cudaEvent_t* ev = instrument ? &op_ev[phase][li * 8] : nullptr;
+            if (instrument) cuda_ok(timing_record(lay_ev[phase][2 * li], cs), "ev");
             cuda_ok(hp::launch_layernorm(x, h1, m, static_cast<int>(h1), L.ln[0], L.ln[1], scr_a,
                                          h1, cs),
                     "ln1");
@@ -390,6 +396,7 @@ struct pipeline::impl {
                     "ln2");
             qlin(L.ops[2], scr_a, h1, m, scr_f, h2, nullptr, HP_EPI_RELU, phase, ev ? ev + 4 : nullptr);
             qlin(L.ops[3], scr_f, h2, m, x, h1, x, HP_EPI_NONE, phase, ev ? ev + 6 : nullptr);
+            if (instrument) cuda_ok(timing_record(lay_ev[phase][2 * li + 1], cs), "ev");
         }
     }
 
@@ -690,6 +697,12 @@ struct pipeline::impl {
             if (ui < 0) continue;
             const unit_ref& u = units[ui];
             const int64_t m = ph == 0 ? prefill_rows(u.index) : group_size[u.index];
+            for (size_t li = 0; li < layers.size(); ++li) {
+                float ms = 0.f;
+                cuda_ok(cudaEventElapsedTime(&ms, lay_ev[ph][2 * li], lay_ev[ph][2 * li + 1]),
+                        "elapsed layer");
+                layer_s[ph][li] = ms * 1e-3;
+            }
             for (size_t li = 0; li < layers.size(); ++li)
                 for (int o = 0; o < 4; ++o) {
                     float ms = 0.f;
@@ -743,7 +756,7 @@ struct pipeline::impl {
         for (void* p : dec_x) f(p);
         for (void* p : fb) f(p);
         f(ws);
-        for (auto* v : {&unit_ev, &recv_ev, &comp_ev, &op_ev[0], &op_ev[1]})
+        for (auto* v : {&unit_ev, &recv_ev, &comp_ev, &op_ev[0], &op_ev[1], &lay_ev[0], &lay_ev[1]})
             for (cudaEvent_t e : *v) cudaEventDestroy(e);
         for (cudaEvent_t e : {ev_t0, ev_t1, ev_fork, ev_join_s, ev_join_r})
             if (e) cudaEventDestroy(e);
@@ -798,6 +811,10 @@ pipesim::stage_cost pipeline::measured_cost() const {
 }
 
 const kernel_stats& pipeline::stats(int phase) const { return p_->kstats[phase ? 1 : 0]; }
+
+const std::vector<double>& pipeline::layer_costs(int phase) const {
+    return p_->layer_s[phase ? 1 : 0];
+}
 
 void pipeline::reset_stats() {
     p_->kstats[0] = kernel_stats{};

@@ -70,6 +70,12 @@ class Pipeline:
         check(lib.hp_pipeline_kernel_stats(self._h, phase, out))
         return {"launches": int(out[0]), "seconds": out[1], "bytes": out[2], "flops": out[3]}
 
+    def layer_costs(self, phase: int) -> list[float]:
+        n = C.c_int64()
+        out = (C.c_double * 256)()
+        check(lib.hp_pipeline_layer_costs(self._h, phase, out, 256, C.byref(n)))
+        return list(out[:n.value])
+
     def info(self):
         out = (C.c_int64 * 4)()
         check(lib.hp_pipeline_info(self._h, out))

@@ -122,8 +122,86 @@ def run(name: str) -> str:
     return f"{name}: {dt:.0f}s bits={doc['layer_bits']} stages={[s['layers'] for s in doc['stages']]} eta={doc['eta']} xi={doc['xi']} optimal={doc['optimal']}"
 
 
+def weak(n_dev: int, base: str = "opt13b_b32_1gpu") -> str:
+    """Weak-scaled pipeline plan for bench.py --gpus N: the configs[1] plan's
+    bit assignment (same 40 layers, same bits) with B = 32 N requests, eta 4,
+    xi 32 -- N decode groups in flight, so every stage has one group to work
+    on -- and layers split into N contiguous stages minimising the maximum
+    per-stage work of one round, 8N prefill micro-batches + 99N decode
+    group-tokens, on the per-layer costs MEASURED on a B200
+    (b200_layer_costs.json, tools/layer_costs.py). NOT a reference-planner output: the planner
+    prefers xi = B (one decode group), which leaves a
+    pipeline nothing to overlap in decode. The objective parts follow the
+    same latency model and recompose exactly (types.cpp:17-24, :118-122)."""
+    src = json.loads((OUT / f"{base}.json").read_text())
+    bits = src["layer_bits"]
+    L, h1, h2 = SHAPES[src["model"]]
+    P = 4 * h1 * h1 + 2 * h1 * h2
+    s, eta, xi = src["workload"]["s"], src["eta"], 32
+    B = 32 * n_dev
+    meas = json.loads((OUT / "b200_layer_costs.json").read_text())
+    assert meas["layer_bits"] == bits and meas["eta"] == eta, "layer costs of another plan"
+    pre, dec = meas["prefill_s"], meas["decode_s"]
+    n_pre = -(-B // eta) // n_dev              # per-device-share of micro-batches
+    n_dec = (src["workload"]["n"] - 1)         # group-tokens per group
+    work = [n_pre * p_ + n_dec * d_ for p_, d_ in zip(pre, dec)]
+    # contiguous min-max partition (DP over split points)
+    INF = float("inf")
+    pref = [0.0]
+    for w_ in work:
+        pref.append(pref[-1] + w_)
+    best = [[INF] * (L + 1) for _ in range(n_dev + 1)]
+    cut = [[0] * (L + 1) for _ in range(n_dev + 1)]
+    best[0][0] = 0.0
+    for j in range(1, n_dev + 1):
+        for e in range(j, L + 1):
+            for b0 in range(j - 1, e):
+                v = max(best[j - 1][b0], pref[e] - pref[b0])
+                if v < best[j][e]:
+                    best[j][e], cut[j][e] = v, b0
+    bounds, e = [], L
+    for j in range(n_dev, 0, -1):
+        bounds.append((cut[j][e], e))
+        e = cut[j][e]
+    bounds.reverse()
+    t_pre = [sum(pre[a:b]) for a, b in bounds]
+    t_dec = [sum(dec[a:b]) for a, b in bounds]
+    omega = {int(r.split(",")[0]): [float(x) for x in r.split(",")[1:]]
+             for r in (OUT / f"{base}.omega.csv").read_text().splitlines()[1:] if r}
+    col = {3: 0, 4: 1, 8: 2, 16: 3}
+    omega_sum = sum(omega[i][col[b]] for i, b in enumerate(bits))
+    theta, n = src["theta"], src["workload"]["n"]
+    bc = lambda u: -(-(B - u) // u)
+    obj = {"t_max_pre": max(t_pre), "t_max_dec": max(t_dec), "t_pre_total": sum(t_pre),
+           "t_dec_total": sum(t_dec), "omega_sum": omega_sum, "theta": theta}
+    obj["total"] = (bc(eta) * obj["t_max_pre"] + bc(xi) * (n - 1) * obj["t_max_dec"]
+                    + obj["t_pre_total"] + obj["t_dec_total"] + theta * omega_sum)
+    name = f"opt13b_b{B}_{n_dev}gpu_weak"
+    doc = dict(src)
+    doc.update({"workload": {"global_bz": B, "s": s, "n": n}, "eta": eta, "xi": xi,
+                "device_order": list(range(n_dev)), "devices": ["b200"] * n_dev,
+                "stages": [{"device_index": j, "device": "b200", "layers": [a, b]}
+                           for j, (a, b) in enumerate(bounds)],
+                "objective": obj, "optimal": False})
+    doc["_fixture"] = {"generator": "tests/golden/make_plans.py weak", "derived_from": base,
+                       "note": weak.__doc__.split("\n\n")[0]}
+    cfg = json.loads((OUT / f"{base}.config.json").read_text())
+    cfg["cluster"]["devices"] = [cfg["cluster"]["devices"][0]] * n_dev
+    cfg["workload"]["B"] = B
+    (OUT / f"{name}.json").write_text(json.dumps(doc, indent=1))
+    (OUT / f"{name}.config.json").write_text(json.dumps(cfg, indent=1))
+    (OUT / f"{name}.omega.csv").write_text((OUT / f"{base}.omega.csv").read_text())
+    (OUT / f"{name}.latency.json").write_text((OUT / f"{base}.latency.json").read_text())
+    return (f"{name}: stages={bounds} work/stage="
+            f"{[round(n_dev * (pref[b] - pref[a]), 3) for a, b in bounds]} s")
+
+
 if __name__ == "__main__":
     OUT.mkdir(exist_ok=True)
+    if sys.argv[1:2] == ["weak"]:
+        for nd in (2, 4, 8):
+            print(weak(nd))
+        sys.exit(0)
     names = sys.argv[1:] or list(CONFIGS)
     with ProcessPoolExecutor(max_workers=min(len(names), 6)) as ex:
         for line in ex.map(run, names):

@@ -134,7 +134,10 @@ def test_protocol_world2_interleaved_groups():
     assert sum(res.values()) == 2 * (4 + 2 * 4)  # each stage: 4 prefill + 2 groups x 4 tokens
 
 
-@pytest.mark.parametrize("name,world", [("opt30b_b32_2gpu", 2), ("opt30b_b32_4gpu", 4)])
+@pytest.mark.parametrize("name,world", [("opt30b_b32_2gpu", 2), ("opt30b_b32_4gpu", 4),
+                                        ("opt13b_b64_2gpu_weak", 2),
+                                        ("opt13b_b128_4gpu_weak", 4),
+                                        ("opt13b_b256_8gpu_weak", 8)])
 def test_protocol_reference_plans(name, world):
     plan = (PLANS / f"{name}.json").read_text()
     model = json.dumps(json.loads((PLANS / f"{name}.config.json").read_text())["model"])
