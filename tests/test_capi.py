@@ -75,3 +75,19 @@ def test_plan_documents_round_trip_and_validate():
     bad["layer_bits"][0] = 5
     with pytest.raises(capi.InvalidArgument):
         capi.check(capi.lib.hp_host_plan_check(json.dumps(bad).encode(), buf, len(buf)))
+
+
+def test_cpp_wrappers_keep_reference_exception_contract(tmp_path):
+    """include/hetplan/{quant,qlinear}.hpp rethrow hp_status as the reference's
+    exception types: invalid_argument / runtime_error."""
+    import subprocess
+    root = Path(__file__).resolve().parents[1]
+    lib = root / "paper_2403_01136_b200" / "libhetplan_b200.so"
+    exe = tmp_path / "wrappers"
+    r = subprocess.run(["/usr/bin/g++", "-std=c++20", "-O1", f"-I{root / 'include'}",
+                        str(root / "tests" / "dropin" / "wrappers_main.cpp"), "-o", str(exe),
+                        f"-L{lib.parent}", "-lhetplan_b200", f"-Wl,-rpath,{lib.parent}"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-3000:]
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0 and "wrappers: ok" in r.stdout, r.stdout + r.stderr
