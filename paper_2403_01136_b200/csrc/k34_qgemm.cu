@@ -192,8 +192,33 @@ struct qgemm_cfg {
 // stg[t][r]; after a named barrier the 128 threads write the tile as 16-byte
 // vectors along n (coalesced), adding the residual in fp32 and rounding once
 // — the same arithmetic as a per-element epilogue, so results are identical.
+// Residual of this thread's store-phase slot (token t0 + tid/8, 16 features
+// at n0 + (tid%8)*16), fetched early so a reducing epilogue overlaps its
+// latency with the partial loads; `ok` = vector path usable.
+struct res16 {
+    uint4 r0, r1;
+    bool ok;
+};
+__device__ __forceinline__ res16 prefetch_res16(const qgemm_args& a, int t0, int n0) {
+    res16 o{};
+    const int tid = threadIdx.x & 127;
+    const int tok = t0 + (tid >> 3);
+    const int n = n0 + (tid & 7) * 16;
+    o.ok = false;
+    if (a.res && tok < a.m && n + 16 <= a.n_out) {
+        const __nv_bfloat16* res = a.res + static_cast<int64_t>(tok) * a.ldr + n;
+        if ((reinterpret_cast<uintptr_t>(res) & 15) == 0) {
+            o.r0 = __ldcg(reinterpret_cast<const uint4*>(res));
+            o.r1 = __ldcg(reinterpret_cast<const uint4*>(res + 8));
+            o.ok = true;
+        }
+    }
+    return o;
+}
+
 __device__ __forceinline__ void stage_store16(const qgemm_args& a, float* stg, int ldst, int r,
-                                              const float (&v)[16], int t0, int n0) {
+                                              const float (&v)[16], int t0, int n0,
+                                              const res16* pre = nullptr) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) stg[i * ldst + r] = v[i];
     asm volatile("bar.sync 2, 128;" ::: "memory");
@@ -220,8 +245,8 @@ __device__ __forceinline__ void stage_store16(const qgemm_args& a, float* stg, i
                          (!res || (reinterpret_cast<uintptr_t>(res) & 15) == 0);
         if (vec) {
             if (res) {
-                const uint4 r0 = *reinterpret_cast<const uint4*>(res);
-                const uint4 r1 = *reinterpret_cast<const uint4*>(res + 8);
+                const uint4 r0 = pre && pre->ok ? pre->r0 : *reinterpret_cast<const uint4*>(res);
+                const uint4 r1 = pre && pre->ok ? pre->r1 : *reinterpret_cast<const uint4*>(res + 8);
                 const __nv_bfloat162* h0 = reinterpret_cast<const __nv_bfloat162*>(&r0);
                 const __nv_bfloat162* h1 = reinterpret_cast<const __nv_bfloat162*>(&r1);
 #pragma unroll
@@ -515,8 +540,12 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
             trace_ev(a, warp == C::kEpiWarp0 && lane == 0 ? 3 : 99, 48 + ut, 1);
             tc_fence_after();
             constexpr bool kSK = BN <= 64;  // stream-K only runs the decode tiles
-            float* part = (kSK && sg.nseg > 1) ? a.partial + ((static_cast<size_t>(sg.tile) * a.maxseg + sg.idx) * 128 + r) * BN
-                                      : nullptr;
+            // partials: [tile][seg][BN/4][128 rows] float4 -- row r is the
+            // thread, so every warp access is 512 contiguous bytes
+            float4* part = (kSK && sg.nseg > 1)
+                               ? reinterpret_cast<float4*>(a.partial) +
+                                     (static_cast<size_t>(sg.tile) * a.maxseg + sg.idx) * (BN / 4) * 128 + r
+                               : nullptr;
 #pragma unroll 1
             for (int c0 = 0; c0 < BN; c0 += 16) {
                 uint32_t v[16];
@@ -525,7 +554,7 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
                 if (kSK && part) {
 #pragma unroll
                     for (int i = 0; i < 16; i += 4)
-                        __stcg(reinterpret_cast<float4*>(part + c0 + i),
+                        __stcg(part + ((c0 + i) / 4) * 128,
                                make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
                                            __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3])));
                 } else {
@@ -541,37 +570,69 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
             trace_ev(a, warp == C::kEpiWarp0 && lane == 0 ? 3 : 99, 48 + ut, 2);
 
             if constexpr (kSK) if (sg.nseg > 1) {
+                const int tr5 = warp == C::kEpiWarp0 && lane == 0 ? 5 : 99;
                 __threadfence();
+                trace_ev(a, tr5, ut, 0);
                 asm volatile("bar.sync 1, 128;" ::: "memory");
                 if (warp == C::kEpiWarp0 && lane == 0)
                     *bcast = atomicAdd(&a.counters[sg.tile], 1u);
                 asm volatile("bar.sync 1, 128;" ::: "memory");
+                trace_ev(a, tr5, ut, 1);
                 if (*bcast == static_cast<unsigned>(sg.nseg - 1)) {
                     __threadfence();
+                    trace_ev(a, tr5, ut, 2);
                     // ordered reduction of all segments of this tile (row r), 16
-                    // tokens at a time (keeps the epilogue within 64 registers)
-                    const float* base = a.partial + (static_cast<size_t>(sg.tile) * a.maxseg * 128 + r) * BN;
+                    // tokens at a time. The partial loads of kRB segments are
+                    // issued together (and the residual with them), so the
+                    // reduction costs ~ceil(nseg/kRB) L2 round trips per chunk,
+                    // not nseg: this CTA is the tile's straggler, on the kernel tail.
+                    constexpr int kRB = 2;  // 4 spills under the 96-register cap
+                    const float4* base = reinterpret_cast<const float4*>(a.partial) +
+                                         static_cast<size_t>(sg.tile) * a.maxseg * (BN / 4) * 128 + r;
 #pragma unroll 1
-                    for (int c0 = 0; c0 < BN; c0 += 16) {
+                    for (int c = 0; c < BN / 16; ++c) {
+                        const int c0 = 16 * c;
+#ifdef HP_RES_PREFETCH
+                        const res16 pre = prefetch_res16(a, mt * BN + c0, nt * 128);
+#endif
                         float f[16];
 #pragma unroll
                         for (int i = 0; i < 16; ++i) f[i] = 0.f;
 #pragma unroll 1
-                        for (int j = 0; j < sg.nseg; ++j) {
-                            const float4* src = reinterpret_cast<const float4*>(
-                                base + static_cast<size_t>(j) * 128 * BN + c0);
+                        for (int jb = 0; jb < sg.nseg; jb += kRB) {
+                            float4 q4[kRB][4];
 #pragma unroll
-                            for (int i = 0; i < 4; ++i) {
-                                const float4 q4 = __ldcg(src + i);
-                                f[4 * i] += q4.x;
-                                f[4 * i + 1] += q4.y;
-                                f[4 * i + 2] += q4.z;
-                                f[4 * i + 3] += q4.w;
+                            for (int jj = 0; jj < kRB; ++jj) {
+                                if (jb + jj < sg.nseg) {
+                                    const float4* src =
+                                        base + (static_cast<size_t>(jb + jj) * (BN / 4) + c0 / 4) * 128;
+#pragma unroll
+                                    for (int i = 0; i < 4; ++i) q4[jj][i] = __ldcg(src + i * 128);
+                                }
                             }
+#pragma unroll
+                            for (int jj = 0; jj < kRB; ++jj) {
+                                if (jb + jj < sg.nseg) {
+#pragma unroll
+                                    for (int i = 0; i < 4; ++i) {
+                                        f[4 * i] += q4[jj][i].x;
+                                        f[4 * i + 1] += q4[jj][i].y;
+                                        f[4 * i + 2] += q4[jj][i].z;
+                                        f[4 * i + 3] += q4[jj][i].w;
+                                    }
+                                }
+                            }
+                            if (jb == 0) trace_ev(a, tr5, 32 + ut, 2 * c);
                         }
+#ifdef HP_RES_PREFETCH
+                        stage_store16(a, stg, C::kStgLd, r, f, mt * BN + c0, nt * 128, &pre);
+#else
                         stage_store16(a, stg, C::kStgLd, r, f, mt * BN + c0, nt * 128);
+#endif
+                        trace_ev(a, tr5, 32 + ut, 2 * c + 1);
                     }
                     if (warp == C::kEpiWarp0 && lane == 0) a.counters[sg.tile] = 0u;
+                    trace_ev(a, tr5, ut, 3);
                 }
                 asm volatile("bar.sync 1, 128;" ::: "memory");
             }

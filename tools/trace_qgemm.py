@@ -54,8 +54,9 @@ def main():
     t0 = t[t > 0].min()
     names = ["producer (start, empty_ok, issued)", "mma (start, full_ok, afull_ok, committed)",
              "dequant w4 (start, full_ok, aempty_ok, arrived)", "epilogue seg (start, tfull_ok, stored, fixup_done) @48..",
-             "dequant w4 detail (codes_loaded, st_issued, st_done, -)", "unused"]
-    for r in range(5):
+             "dequant w4 detail (codes_loaded, st_issued, st_done, -)",
+             "fixup by segment (fence1_done, ticket, fence2_done[last], reduced[last])"]
+    for r in range(6):
         print(names[r])
         for it in range(0, 64):
             row = t[r, it]
