@@ -138,6 +138,34 @@ hp_status hp_qlinear(const hp_qweight* w, const void* x, int64_t ldx,
                      int64_t ldr, int epilogue, int phase, void* workspace,
                      size_t workspace_bytes, hp_stream stream);
 
+/* K3 fused — one decode step of a stack of OPT decoder layers in ONE
+ * persistent kernel launch (the per-op hp_qlinear launches' arithmetic,
+ * bit-identical, without a pipeline drain at every op boundary):
+ *   for each layer: a = LN1(x); qkv = a·Wqkvᵀ; x += qkv[:, 2h1:3h1]·Woutᵀ;
+ *                   a = LN2(x); f = relu(a·Wfc1ᵀ); x += f·Wfc2ᵀ
+ * (self-only attention: the attention output is the V slice). x [m × h1]
+ * bf16 device, updated in place, m <= 32. All layers share one scheme; bits
+ * may differ per layer. ln[4] = LN1 gamma, beta, LN2 gamma, beta (bf16 [h1]).
+ * The plan owns its scratch, op table, TMA descriptors and stream-K
+ * workspace; run() is one kernel launch (CUDA-graph capturable).         */
+/* Glue (decoder-layer LayerNorm, glue.cu): y[r] = LN(x[r])*gamma + beta for
+ * r < rows, fp32 statistics, eps 1e-5; h % 8 == 0, 16-byte aligned rows.  */
+hp_status hp_layernorm(const void* x, int64_t ldx, int64_t rows, int64_t h, const void* gamma,
+                       const void* beta, void* y, int64_t ldy, hp_stream stream);
+
+typedef struct {
+    hp_qweight ops[4];   /* qkv [3h1 × h1], out [h1 × h1], fc1 [h2 × h1], fc2 [h1 × h2] */
+    const void* ln[4];
+} hp_decoder_layer;
+typedef struct hp_decode_plan hp_decode_plan;
+hp_status hp_decode_plan_create(const hp_decoder_layer* layers, int n_layers, void* x,
+                                int64_t m, hp_decode_plan** out);
+hp_status hp_decode_plan_run(hp_decode_plan* p, hp_stream stream);
+/* {weight bytes streamed per run, algorithmic bytes per run (weights +
+ *  activations), ops, grid}                                */
+hp_status hp_decode_plan_info(hp_decode_plan* p, double* out4);
+void hp_decode_plan_destroy(hp_decode_plan* p);
+
 /* ---- pipeline executor (one process per GPU, NCCL P2P at boundaries) ----
  * plan_json: a plan document (schema of hetplan_main.cpp:190-224, loaded by
  * hetplan::plan_io); stage `rank` of the plan runs on this process's current

@@ -48,6 +48,10 @@ class hp_qweight(C.Structure):
     ]
 
 
+class hp_decoder_layer(C.Structure):
+    _fields_ = [("ops", hp_qweight * 4), ("ln", C.c_void_p * 4)]
+
+
 class hp_pipeline_options(C.Structure):
     _fields_ = [
         ("scheme", C.c_int32),
@@ -102,6 +106,11 @@ def _load() -> C.CDLL:
         "hp_pipeline_layer_costs": (i32, [v, i32, P(d), i64, P(i64)]),
         "hp_pipeline_info": (i32, [v, P(i64)]),
         "hp_pipeline_destroy": (None, [v]),
+        "hp_layernorm": (i32, [v, i64, i64, i64, v, v, v, i64, v]),
+        "hp_decode_plan_create": (i32, [P(hp_decoder_layer), i32, v, i64, P(v)]),
+        "hp_decode_plan_run": (i32, [v, v]),
+        "hp_decode_plan_info": (i32, [v, P(d)]),
+        "hp_decode_plan_destroy": (None, [v]),
     })
     optional = {}
     for name, (res, args) in list(sig.items()) + list(optional.items()):
@@ -125,6 +134,7 @@ EXPORTED = [
     "hp_host_make_schedule", "hp_host_simulate", "hp_host_plan_check", "hp_host_unit_order", "hp_set_sm_budget", "hp_set_pdl",
     "hp_nccl_unique_id", "hp_pipeline_create", "hp_pipeline_run", "hp_pipeline_stage_costs",
     "hp_pipeline_kernel_stats", "hp_pipeline_layer_costs", "hp_pipeline_info", "hp_pipeline_destroy",
+    "hp_layernorm", "hp_decode_plan_create", "hp_decode_plan_run", "hp_decode_plan_info", "hp_decode_plan_destroy",
 ]
 
 

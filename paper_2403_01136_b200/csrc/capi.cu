@@ -6,9 +6,12 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
+#include <algorithm>
 
 #include "hp_capi.h"
 #include "layout.cuh"
@@ -37,6 +40,32 @@ struct qgemm_plan {
     int64_t total;
 };
 qgemm_plan plan_qgemm(int64_t n_out, int64_t k_in, int64_t m, int phase);
+struct dstage_op {
+    const uint8_t* packed;
+    const float* scale;
+    const float* zero;
+    void* y;
+    const void* res;
+    const CUtensorMap* tmap;
+    int64_t ldy, ldr;
+    int total;
+    int kind;
+    int bits, n_out, k_in, G, NT, maxseg, epi, sps;
+    unsigned wait;
+    const void* ln_x;
+    const void* gamma;
+    const void* beta;
+    void* ln_y;
+    int64_t ln_ldx, ln_ldy;
+    int h;
+    int P;
+};
+static_assert(sizeof(dstage_op) == 168, "dstage_op layout is shared by k3_stage.cu and capi.cu");
+int dstage_grid();
+cudaError_t launch_layernorm(const void* x, int64_t ldx, int64_t rows, int h, const void* gamma,
+                             const void* beta, void* y, int64_t ldy, cudaStream_t st);
+cudaError_t launch_dstage(const dstage_op* ops, int nops, int m, bool sym, unsigned* sync,
+                          unsigned* counters, float* partial, int grid, cudaStream_t st);
 int slices_per_stage(int bits, int bn);
 cudaError_t launch_qgemm(const CUtensorMap& map, const qgemm_plan& p, int bits, bool sym,
                          const void* packed, const float* scale, const float* zero,
@@ -276,6 +305,203 @@ hp_status hp_qlinear(const hp_qweight* w, const void* x, int64_t ldx, int64_t m,
                                         residual, ldr, epilogue, workspace,
                                         static_cast<cudaStream_t>(stream)),
                        "qlinear");
+}
+
+hp_status hp_layernorm(const void* x, int64_t ldx, int64_t rows, int64_t h, const void* gamma,
+                       const void* beta, void* y, int64_t ldy, hp_stream stream) {
+    if (!x || !gamma || !beta || !y) return fail(HP_EINVAL, "layernorm: NULL pointer");
+    if (rows <= 0 || h <= 0 || h > 16384 || ldx < h || ldy < h)
+        return fail(HP_EINVAL, "layernorm: bad shape");
+    if (hp_status s = need_device()) return s;
+    return cuda_status(hp::launch_layernorm(x, ldx, rows, static_cast<int>(h), gamma, beta, y, ldy,
+                                            static_cast<cudaStream_t>(stream)),
+                       "layernorm");
+}
+
+struct hp_decode_plan {
+    std::vector<void*> allocs;
+    hp::dstage_op* d_ops = nullptr;
+    int nops = 0;
+    int m = 0;
+    bool sym = true;
+    unsigned* sync = nullptr;
+    unsigned* counters = nullptr;
+    float* partial = nullptr;
+    int grid = 0;
+    double weight_bytes = 0, alg_bytes = 0;
+    void* scratch[3] = {nullptr, nullptr, nullptr};
+};
+
+/* debug (not in the ABI header): scratch buffers a, qkv, f of a plan */
+void hp_decode_plan_debug_scratch(hp_decode_plan* p, void** out3) {
+    for (int i = 0; i < 3; ++i) out3[i] = p->scratch[i];
+}
+
+hp_status hp_decode_plan_create(const hp_decoder_layer* layers, int n_layers, void* x,
+                                int64_t m, hp_decode_plan** out) {
+    if (!out) return fail(HP_EINVAL, "decode_plan: NULL out");
+    *out = nullptr;
+    if (!layers || n_layers <= 0) return fail(HP_EINVAL, "decode_plan: no layers");
+    if (!x || (reinterpret_cast<uintptr_t>(x) & 15)) return fail(HP_EINVAL, "decode_plan: x must be 16-byte aligned");
+    if (m <= 0 || m > 32) return fail(HP_EINVAL, "decode_plan: m must be in [1, 32]");
+    const int64_t h1 = layers[0].ops[1].n_out, h2 = layers[0].ops[2].n_out;
+    const int scheme = layers[0].ops[0].scheme;
+    if (h1 <= 0 || h1 % 128 || h2 % 128 || h1 > 16384)
+        return fail(HP_EINVAL, "decode_plan: h1, h2 must be multiples of 128 (h1 <= 16384)");
+    for (int l = 0; l < n_layers; ++l) {
+        const hp_decoder_layer& L = layers[l];
+        const int64_t shp[4][2] = {{3 * h1, h1}, {h1, h1}, {h2, h1}, {h1, h2}};
+        for (int o = 0; o < 4; ++o) {
+            if (hp_status s = check_qweight(&L.ops[o])) return s;
+            if (L.ops[o].n_out != shp[o][0] || L.ops[o].k_in != shp[o][1])
+                return fail(HP_EINVAL, "decode_plan: layer " + std::to_string(l) + " op " +
+                                           std::to_string(o) + " has the wrong shape");
+            if (L.ops[o].scheme != scheme) return fail(HP_EINVAL, "decode_plan: mixed schemes");
+        }
+        for (int j = 0; j < 4; ++j)
+            if (!L.ln[j] || (reinterpret_cast<uintptr_t>(L.ln[j]) & 15))
+                return fail(HP_EINVAL, "decode_plan: LN parameters must be 16-byte aligned");
+    }
+    if (hp_status s = need_device()) return s;
+    auto* p = new hp_decode_plan();
+    auto cleanup = [&](hp_status s) {
+        hp_decode_plan_destroy(p);
+        return s;
+    };
+    auto dalloc = [&](size_t bytes) -> void* {
+        void* q = nullptr;
+        if (cudaMalloc(&q, std::max<size_t>(bytes, 256)) != cudaSuccess) return nullptr;
+        p->allocs.push_back(q);
+        return q;
+    };
+    p->m = static_cast<int>(m);
+    p->sym = scheme == HP_SYMMETRIC;
+    p->grid = hp::dstage_grid();
+    void* scr_a = dalloc(m * h1 * 2);
+    void* scr_qkv = dalloc(m * 3 * h1 * 2);
+    void* scr_f = dalloc(m * h2 * 2);
+    if (!scr_a || !scr_qkv || !scr_f) return cleanup(fail(HP_ECUDA, "decode_plan: cudaMalloc"));
+    p->scratch[0] = scr_a;
+    p->scratch[1] = scr_qkv;
+    p->scratch[2] = scr_f;
+    // host op table + tensor maps
+    std::vector<hp::dstage_op> ops;
+    std::vector<CUtensorMap> maps;
+    std::vector<int> map_of;  // op index -> map index
+    size_t part_bytes = 0;
+    int max_nt = 1;
+    unsigned done = 0;
+    auto gemm = [&](const hp_qweight& w, const void* xin, int64_t ldx, void* y, int64_t ldy,
+                    const void* res, int epi) -> hp_status {
+        hp::dstage_op op{};
+        op.kind = 0;
+        op.bits = w.bits;
+        op.packed = static_cast<const uint8_t*>(w.packed);
+        op.scale = w.scale;
+        op.zero = w.zero;
+        op.n_out = static_cast<int>(w.n_out);
+        op.k_in = static_cast<int>(w.k_in);
+        op.G = static_cast<int>(hp::ceil_div64(w.k_in, 128));
+        op.NT = static_cast<int>(hp::ceil_div64(w.n_out, 128));
+        op.total = op.NT * op.G;
+        const int64_t grid = std::min<int64_t>(p->grid, op.total);
+        op.P = static_cast<int>(grid);
+        const int64_t per = op.total / grid;
+        op.maxseg = static_cast<int>(std::min<int64_t>((op.G + per - 1) / per + 1, grid));
+        op.sps = w.bits <= 4 ? 8 : (w.bits == 8 ? 4 : 2);
+        op.y = y;
+        op.ldy = ldy;
+        op.res = res;
+        op.ldr = res ? ldy : 0;
+        op.epi = epi;
+        op.wait = done;
+        done += static_cast<unsigned>(op.NT);
+        CUtensorMap map;
+        if (hp_status s = make_act_map(&map, xin, w.k_in, m, ldx, 32, op.sps / 2)) return s;
+        map_of.push_back(static_cast<int>(maps.size()));
+        maps.push_back(map);
+        ops.push_back(op);
+        part_bytes = std::max(part_bytes, static_cast<size_t>(op.NT) * op.maxseg * 128 * 32 * 4);
+        max_nt = std::max(max_nt, op.NT);
+        p->weight_bytes += static_cast<double>(hp_packed_bytes(w.n_out, w.k_in, w.bits)) +
+                           (w.bits == 16 ? 0.0 : 4.0 * hp_scale_count(w.n_out, w.k_in) *
+                                                     (w.scheme == HP_SYMMETRIC ? 1 : 2));
+        p->alg_bytes += 2.0 * m * (w.n_out + w.k_in);
+        return HP_OK;
+    };
+    auto ln = [&](const void* gamma, const void* beta) {
+        hp::dstage_op op{};
+        op.kind = 1;
+        op.ln_x = x;
+        op.ln_ldx = h1;
+        op.ln_y = scr_a;
+        op.ln_ldy = h1;
+        op.gamma = gamma;
+        op.beta = beta;
+        op.h = static_cast<int>(h1);
+        op.wait = done;
+        done += static_cast<unsigned>(m);
+        map_of.push_back(-1);
+        ops.push_back(op);
+    };
+    for (int l = 0; l < n_layers; ++l) {
+        const hp_decoder_layer& L = layers[l];
+        ln(L.ln[0], L.ln[1]);
+        if (hp_status s = gemm(L.ops[0], scr_a, h1, scr_qkv, 3 * h1, nullptr, 0)) return cleanup(s);
+        if (hp_status s = gemm(L.ops[1], static_cast<char*>(scr_qkv) + 2 * h1 * 2, 3 * h1, x, h1, x, 0))
+            return cleanup(s);
+        ln(L.ln[2], L.ln[3]);
+        if (hp_status s = gemm(L.ops[2], scr_a, h1, scr_f, h2, nullptr, HP_EPI_RELU)) return cleanup(s);
+        if (hp_status s = gemm(L.ops[3], scr_f, h2, x, h1, x, 0)) return cleanup(s);
+    }
+    p->alg_bytes += p->weight_bytes;
+    p->nops = static_cast<int>(ops.size());
+    // device image: [maps (64-B aligned)] [ops] [sync + counters] [partials]
+    const size_t maps_bytes = maps.size() * sizeof(CUtensorMap);
+    const size_t ops_off = (maps_bytes + 255) / 256 * 256;
+    const size_t ops_bytes = ops.size() * sizeof(hp::dstage_op);
+    const size_t sync_off = (ops_off + ops_bytes + 255) / 256 * 256;
+    const size_t sync_bytes = (2 + static_cast<size_t>(max_nt)) * sizeof(unsigned);
+    const size_t part_off = (sync_off + sync_bytes + 255) / 256 * 256;
+    auto* base = static_cast<char*>(dalloc(part_off + part_bytes));
+    if (!base) return cleanup(fail(HP_ECUDA, "decode_plan: cudaMalloc"));
+    auto* dmaps = reinterpret_cast<CUtensorMap*>(base);
+    for (size_t i = 0; i < ops.size(); ++i)
+        if (map_of[i] >= 0) ops[i].tmap = dmaps + map_of[i];
+    p->d_ops = reinterpret_cast<hp::dstage_op*>(base + ops_off);
+    p->sync = reinterpret_cast<unsigned*>(base + sync_off);
+    p->counters = p->sync + 2;
+    p->partial = reinterpret_cast<float*>(base + part_off);
+    if (cudaMemcpy(dmaps, maps.data(), maps_bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(p->d_ops, ops.data(), ops_bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemset(p->sync, 0, sync_bytes) != cudaSuccess)
+        return cleanup(fail(HP_ECUDA, "decode_plan: upload"));
+    *out = p;
+    return HP_OK;
+}
+
+hp_status hp_decode_plan_run(hp_decode_plan* p, hp_stream stream) {
+    if (!p) return fail(HP_EINVAL, "decode_plan_run: NULL plan");
+    int nops = p->nops;
+    if (const char* e = getenv("HP_DSTAGE_NOPS")) nops = std::min(nops, atoi(e));  // debug
+    return cuda_status(hp::launch_dstage(p->d_ops, nops, p->m, p->sym, p->sync, p->counters,
+                                         p->partial, p->grid, static_cast<cudaStream_t>(stream)),
+                       "decode_plan_run");
+}
+
+hp_status hp_decode_plan_info(hp_decode_plan* p, double* out4) {
+    if (!p || !out4) return fail(HP_EINVAL, "decode_plan_info: NULL argument");
+    out4[0] = p->weight_bytes;
+    out4[1] = p->alg_bytes;
+    out4[2] = p->nops;
+    out4[3] = p->grid;
+    return HP_OK;
+}
+
+void hp_decode_plan_destroy(hp_decode_plan* p) {
+    if (!p) return;
+    for (void* q : p->allocs) cudaFree(q);
+    delete p;
 }
 
 }  // extern "C"

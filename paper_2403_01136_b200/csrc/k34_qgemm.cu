@@ -31,6 +31,13 @@
 #include "layout.cuh"
 #include "sm100.cuh"
 
+#ifndef HP_DEC_SPS
+#define HP_DEC_SPS 8
+#endif
+#ifndef HP_CR_CAP
+#define HP_CR_CAP 12
+#endif
+
 namespace hp {
 
 // Persistent-grid cap: leave SMs to concurrent NCCL kernels (pipeline runs).
@@ -163,7 +170,7 @@ struct qgemm_cfg {
     // ring (L2-resident x, released by the MMA) is shallow.
     static constexpr int kBudget = 186 * 1024;
     static constexpr int BR = BN <= 64 ? 3 : (BN <= 128 ? 6 : 4);
-    static constexpr int CR_ = (kBudget - BR * kB) / kCS > 12 ? 12 : (kBudget - BR * kB) / kCS;
+    static constexpr int CR_ = (kBudget - BR * kB) / kCS > HP_CR_CAP ? HP_CR_CAP : (kBudget - BR * kB) / kCS;
     // Round-robin consumers wait only on their own stages, so every ring slot
     // they consume must always belong to the same warpgroup (depth % DWG ==
     // 0); otherwise an mbarrier parity wait could alias another phase.
@@ -425,14 +432,12 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
                 tc_fence_after();
                 const uint32_t bbase = smem_u32(stage_b(s));
                 const uint32_t abase = tmem + C::A0 + as * C::ACOLS;
+                const uint64_t bdesc0 = umma_desc_sw128(bbase);
 #pragma unroll
-                for (int j = 0; j < 2 * SPS; ++j) {
-                    if (j < 2 * nsl) {
-                        const uint64_t bdesc =
-                            umma_desc_sw128(bbase + (j >> 2) * (BN * 128) + (j & 3) * 32);
-                        mma_ts_elect(d_tmem, abase + j * 8, bdesc, idesc,
-                                     (sl > 4 * sg.g0 || j > 0) ? 1u : 0u);
-                    }
+                for (int q = 0; q < SPS / 2; ++q) {  // 64-k sub-tiles (4 MMAs each)
+                    if (2 * q < nsl)
+                        mma_ts_x4_elect(d_tmem, abase + q * 32, bdesc0 + q * (BN * 8), idesc,
+                                        (sl > 4 * sg.g0 || q > 0) ? 1u : 0u);
                 }
                 tc_commit_elect(&empty_b[s]);
                 tc_commit_elect(&aempty[as]);
@@ -667,9 +672,9 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
 // amortise the per-stage barrier/issue work; prefill moves half a group so
 // the [BN x 64] activation tile per stage is small and the pipeline deep.
 template <int BITS, int BN>
-constexpr int kSlicesPerStage = BN <= 64 ? (BITS >= 8 ? 4 : 8) : 2;
+constexpr int kSlicesPerStage = BN <= 64 ? (BITS >= 8 ? 4 : HP_DEC_SPS) : 2;
 
-int slices_per_stage(int bits, int bn) { return bn <= 64 ? (bits >= 8 ? 4 : 8) : 2; }
+int slices_per_stage(int bits, int bn) { return bn <= 64 ? (bits >= 8 ? 4 : HP_DEC_SPS) : 2; }
 
 namespace {
 
@@ -733,6 +738,8 @@ struct qgemm_plan {
     int64_t total;
 };
 
+constexpr size_t kTicketBytes = 16384;  // stream-K tile tickets: <= 4096 tiles
+
 qgemm_plan plan_qgemm(int64_t n_out, int64_t k_in, int64_t m, int phase) {
     qgemm_plan p{};
     const int G = static_cast<int>(ceil_div64(k_in, 128));
@@ -752,13 +759,16 @@ qgemm_plan plan_qgemm(int64_t n_out, int64_t k_in, int64_t m, int phase) {
     p.maxseg = 1;
     p.total = tiles * G;
     // stream-K when whole tiles would leave SMs idle or unbalanced
-    p.stream_k = (phase == 1 && tiles % sms != 0) ? 1 : 0;
+    p.stream_k = (phase == 1 && tiles % sms != 0 && tiles <= static_cast<int64_t>(kTicketBytes / 4)) ? 1 : 0;
     if (p.stream_k) {
         p.grid = static_cast<int>(p.total < sms ? p.total : sms);
         const int64_t per = p.total / p.grid;  // >= 1 group-step per CTA
         p.maxseg = static_cast<int>((G + per - 1) / per) + 1;
         if (p.maxseg > p.grid) p.maxseg = p.grid;
-        p.workspace = 256 + (static_cast<size_t>(tiles) * sizeof(unsigned) + 255) / 256 * 256 +
+        // The tile-ticket region has a FIXED size: one workspace serves ops
+        // of different tile counts, and a region sized per op would put one
+        // op's partials over another op's (never re-zeroed) tickets.
+        p.workspace = kTicketBytes +
                       static_cast<size_t>(tiles) * p.maxseg * 128 * p.bn * sizeof(float);
     } else {
         p.grid = static_cast<int>(tiles < sms ? tiles : sms);
@@ -811,7 +821,7 @@ cudaError_t launch_qgemm(const CUtensorMap& map, const qgemm_plan& p, int bits,
         auto* base = static_cast<uint8_t*>(workspace);
         a.counters = reinterpret_cast<unsigned*>(base);
         a.partial = reinterpret_cast<float*>(
-            base + 256 + ((static_cast<size_t>(p.mt) * a.NT * sizeof(unsigned) + 255) / 256) * 256);
+            base + kTicketBytes);
     }
     switch (p.bn) {
         case 16: return dispatch_bits<16>(bits, sym, map, a, p.grid, st);

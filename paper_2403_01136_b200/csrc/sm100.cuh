@@ -38,34 +38,49 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
                  : "memory");
 }
+// Waits pass a suspend-time hint: a warp whose phase is not complete is
+// parked by the hardware (until the phase flips or the hint expires) instead
+// of re-issuing try_wait + branch + vote. Without it the idle roles (epilogue
+// warps waiting for a stream-K accumulator, the round-robin dequant
+// warpgroups waiting for their turn) spent ~20% of all issue slots spinning
+// (ncu, 4-bit decode: BRA+SYNCS+VOTE 24M of 114M instructions).
+#ifndef HP_MBAR_SUSPEND_NS
+#define HP_MBAR_SUSPEND_NS 0x989680
+#endif
+__device__ __forceinline__ uint32_t mbar_try_wait(uint32_t a, uint32_t parity) {
+    uint32_t done;
+#if HP_MBAR_SUSPEND_NS > 0
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity), "n"(HP_MBAR_SUSPEND_NS)
+        : "memory");
+#else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+#endif
+    return done;
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
-    uint32_t done;
-    do {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(a), "r"(parity)
-            : "memory");
-    } while (!done);
+    while (!mbar_try_wait(a, parity)) {
+    }
 }
 
 // Warp-collective wait: the exit condition is made warp-uniform (vote), so
-// code after it stays on the uniform datapath.
+// the caller stays on the uniform datapath.
 __device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
-    uint32_t done;
-    do {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(a), "r"(parity)
-            : "memory");
-    } while (!__all_sync(0xffffffffu, done));
+    while (!__all_sync(0xffffffffu, mbar_try_wait(a, parity))) {
+    }
 }
 
 // ---- programmatic dependent launch ------------------------------------------
@@ -139,6 +154,27 @@ __device__ __forceinline__ void mma_ts_elect(uint32_t d_tmem, uint32_t a_tmem, u
         "setp.ne.b32 q, %4, 0;\n\t"
         "elect.sync _|p, 0xffffffff;\n\t"
         "@p tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, q;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// Four MMAs over one 64-k swizzled sub-tile (k16 steps: A +8 TMEM columns,
+// B descriptor start +32 B) from ONE elect and one asm block: the issuing
+// warp spends ~10 instructions per 4 MMAs instead of ~13 per MMA, which
+// mattered in decode where the MMA warp competes for issue slots with 12
+// dequant warps (trace: 16 MMAs took 0.35 us to issue per stage).
+__device__ __forceinline__ void mma_ts_x4_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                                uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, q, t;\n\t.reg .b64 d1, d2, d3;\n\t.reg .b32 a1, a2, a3;\n\t"
+        "setp.ne.b32 q, %4, 0;\n\t"
+        "setp.eq.b32 t, 0, 0;\n\t"
+        "add.s64 d1, %2, 2;\n\tadd.s64 d2, %2, 4;\n\tadd.s64 d3, %2, 6;\n\t"
+        "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "@p tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, q;\n\t"
+        "@p tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], d1, %3, t;\n\t"
+        "@p tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], d2, %3, t;\n\t"
+        "@p tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], d3, %3, t;\n\t}" ::"r"(d_tmem),
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }

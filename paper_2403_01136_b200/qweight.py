@@ -169,3 +169,41 @@ def qlinear(qw: QuantizedWeight, x: torch.Tensor, phase: int = capi.HP_DECODE,
                          capi.HP_EPI_RELU if relu else capi.HP_EPI_NONE, phase,
                          _ptr(buf), need, _stream(stream)))
     return out
+
+
+class DecodePlan:
+    """K3 fused: one decode step of a decoder-layer stack in one persistent
+    kernel (hp_decode_plan_*). layers: [(qkv, out, fc1, fc2), (ln1_g, ln1_b,
+    ln2_g, ln2_b)] per layer; x [m x h1] bf16 is updated in place by run()."""
+
+    def __init__(self, layers, x: torch.Tensor):
+        assert x.dtype == torch.bfloat16 and x.is_cuda and x.is_contiguous()
+        self._keep = (layers, x)
+        arr = (capi.hp_decoder_layer * len(layers))()
+        for i, (ops, lns) in enumerate(layers):
+            for o in range(4):
+                arr[i].ops[o] = ops[o].c
+            for j in range(4):
+                arr[i].ln[j] = lns[j].data_ptr()
+        h = C.c_void_p()
+        check(lib.hp_decode_plan_create(arr, len(layers), x.data_ptr(), x.shape[0], C.byref(h)))
+        self.h = h
+
+    def run(self, stream=None) -> None:
+        check(lib.hp_decode_plan_run(self.h, _stream(stream)))
+
+    def info(self) -> dict:
+        out = (C.c_double * 4)()
+        check(lib.hp_decode_plan_info(self.h, out))
+        return {"weight_bytes": out[0], "alg_bytes": out[1], "ops": int(out[2]), "grid": int(out[3])}
+
+    def close(self) -> None:
+        if self.h:
+            lib.hp_decode_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -138,3 +138,23 @@ def test_large_shape_decode(cuda, bits):
     got = qweight.qlinear(qw, x, phase=1).float()
     e = float((got - ref).abs().max() / ref.abs().max())
     assert e <= TOL
+
+
+def test_shared_workspace_across_tile_counts(cuda):
+    """One split-K workspace serves ops with different tile counts (the
+    pipeline shares one per stage): an op with few tiles (large partial
+    region start) must not leave data in another op's tile tickets.
+    Regression: out-proj [5120 x 5120] (40 tiles) before fc1 [20480 x 5120]
+    (160 tiles, > 148 SMs) corrupted fc1's split tiles >= 128."""
+    import torch
+    from paper_2403_01136_b200 import qweight
+    g = torch.Generator(device="cpu").manual_seed(7)
+    small = qweight.quantize((torch.randn(5120, 5120, generator=g) * 0.02).to(torch.bfloat16).to(cuda), 4)
+    big = qweight.quantize((torch.randn(20480, 5120, generator=g) * 0.02).to(torch.bfloat16).to(cuda), 4)
+    x = torch.randn(32, 5120, generator=g).to(torch.bfloat16).to(cuda)
+    fresh = qweight.qlinear(big, x, workspace=qweight.Workspace(cuda))
+    ws = qweight.Workspace(cuda)
+    qweight.qlinear(small, x, workspace=ws)
+    chained = qweight.qlinear(big, x, workspace=ws)
+    torch.cuda.synchronize()
+    assert torch.equal(fresh, chained)
