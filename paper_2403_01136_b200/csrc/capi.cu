@@ -59,13 +59,18 @@ struct dstage_op {
     int64_t ln_ldx, ln_ldy;
     int h;
     int P;
+    const unsigned* dep_flags;
+    unsigned* out_flags;
+    int dep_off;
+    int pbuf;
 };
-static_assert(sizeof(dstage_op) == 168, "dstage_op layout is shared by k3_stage.cu and capi.cu");
+static_assert(sizeof(dstage_op) == 192, "dstage_op layout is shared by k3_stage.cu and capi.cu");
 int dstage_grid();
 cudaError_t launch_layernorm(const void* x, int64_t ldx, int64_t rows, int h, const void* gamma,
                              const void* beta, void* y, int64_t ldy, cudaStream_t st);
-cudaError_t launch_dstage(const dstage_op* ops, int nops, int m, bool sym, unsigned* sync,
-                          unsigned* counters, float* partial, int grid, cudaStream_t st);
+cudaError_t launch_dstage(const dstage_op* ops, int nops, int m, int bits, bool sym,
+                          unsigned long long* sync, unsigned long long units, unsigned* const counters[2],
+                          float* const partial[2], int grid, cudaStream_t st);
 int slices_per_stage(int bits, int bn);
 cudaError_t launch_qgemm(const CUtensorMap& map, const qgemm_plan& p, int bits, bool sym,
                          const void* packed, const float* scale, const float* zero,
@@ -319,14 +324,19 @@ hp_status hp_layernorm(const void* x, int64_t ldx, int64_t rows, int64_t h, cons
 }
 
 struct hp_decode_plan {
+    struct run {  // consecutive layers of one bit width = one kernel launch
+        int op0, nops, bits;
+        unsigned long long units;
+        unsigned long long* sync;
+    };
     std::vector<void*> allocs;
+    std::vector<run> runs;
     hp::dstage_op* d_ops = nullptr;
     int nops = 0;
     int m = 0;
     bool sym = true;
-    unsigned* sync = nullptr;
-    unsigned* counters = nullptr;
-    float* partial = nullptr;
+    unsigned* counters[2] = {nullptr, nullptr};
+    float* partial[2] = {nullptr, nullptr};
     int grid = 0;
     double weight_bytes = 0, alg_bytes = 0;
     void* scratch[3] = {nullptr, nullptr, nullptr};
@@ -388,11 +398,12 @@ hp_status hp_decode_plan_create(const hp_decoder_layer* layers, int n_layers, vo
     std::vector<hp::dstage_op> ops;
     std::vector<CUtensorMap> maps;
     std::vector<int> map_of;  // op index -> map index
+    std::vector<std::pair<int, int>> flag_of;  // op index -> (flags offset, count) or (-1, 0)
     size_t part_bytes = 0;
-    int max_nt = 1;
-    unsigned done = 0;
+    int max_nt = 1, nflags = 0, ngemm = 0;
+    unsigned done = 0;  // units of the current run so far
     auto gemm = [&](const hp_qweight& w, const void* xin, int64_t ldx, void* y, int64_t ldy,
-                    const void* res, int epi) -> hp_status {
+                    const void* res, int epi, bool flags_out, int dep_op, int dep_off) -> hp_status {
         hp::dstage_op op{};
         op.kind = 0;
         op.bits = w.bits;
@@ -415,11 +426,16 @@ hp_status hp_decode_plan_create(const hp_decoder_layer* layers, int n_layers, vo
         op.ldr = res ? ldy : 0;
         op.epi = epi;
         op.wait = done;
+        op.pbuf = (ngemm++) & 1;
+        op.dep_off = dep_off;
         done += static_cast<unsigned>(op.NT);
         CUtensorMap map;
         if (hp_status s = make_act_map(&map, xin, w.k_in, m, ldx, 32, op.sps / 2)) return s;
         map_of.push_back(static_cast<int>(maps.size()));
         maps.push_back(map);
+        // flags resolved to device pointers after the upload
+        flag_of.push_back(flags_out ? std::make_pair(nflags, op.NT) : std::make_pair(-1, dep_op));
+        if (flags_out) nflags += op.NT;
         ops.push_back(op);
         part_bytes = std::max(part_bytes, static_cast<size_t>(op.NT) * op.maxseg * 128 * 32 * 4);
         max_nt = std::max(max_nt, op.NT);
@@ -442,39 +458,72 @@ hp_status hp_decode_plan_create(const hp_decoder_layer* layers, int n_layers, vo
         op.wait = done;
         done += static_cast<unsigned>(m);
         map_of.push_back(-1);
+        flag_of.push_back({-1, -1});
         ops.push_back(op);
     };
+    std::vector<int> dep_of;  // op -> producing op index for dataflow edges (or -1)
     for (int l = 0; l < n_layers; ++l) {
         const hp_decoder_layer& L = layers[l];
+        if (l == 0 || L.ops[0].bits != layers[l - 1].ops[0].bits) {  // new run: a kernel boundary
+            if (!p->runs.empty()) {
+                p->runs.back().nops = static_cast<int>(ops.size()) - p->runs.back().op0;
+                p->runs.back().units = done;
+            }
+            p->runs.push_back({static_cast<int>(ops.size()), 0, L.ops[0].bits, 0, nullptr});
+            done = 0;
+        }
+        for (int o = 1; o < 4; ++o)
+            if (L.ops[o].bits != L.ops[0].bits)
+                return cleanup(fail(HP_EINVAL, "decode_plan: the four ops of a layer must share a bit width"));
+        const int i0 = static_cast<int>(ops.size());
         ln(L.ln[0], L.ln[1]);
-        if (hp_status s = gemm(L.ops[0], scr_a, h1, scr_qkv, 3 * h1, nullptr, 0)) return cleanup(s);
-        if (hp_status s = gemm(L.ops[1], static_cast<char*>(scr_qkv) + 2 * h1 * 2, 3 * h1, x, h1, x, 0))
+        if (hp_status s = gemm(L.ops[0], scr_a, h1, scr_qkv, 3 * h1, nullptr, 0, true, -1, 0)) return cleanup(s);
+        // out-proj reads the V slice: qkv output tiles [2 h1/128, 3 h1/128)
+        if (hp_status s = gemm(L.ops[1], static_cast<char*>(scr_qkv) + 2 * h1 * 2, 3 * h1, x, h1, x, 0, false,
+                               i0 + 1, static_cast<int>(2 * h1 / 128)))
             return cleanup(s);
         ln(L.ln[2], L.ln[3]);
-        if (hp_status s = gemm(L.ops[2], scr_a, h1, scr_f, h2, nullptr, HP_EPI_RELU)) return cleanup(s);
-        if (hp_status s = gemm(L.ops[3], scr_f, h2, x, h1, x, 0)) return cleanup(s);
+        if (hp_status s = gemm(L.ops[2], scr_a, h1, scr_f, h2, nullptr, HP_EPI_RELU, true, -1, 0)) return cleanup(s);
+        if (hp_status s = gemm(L.ops[3], scr_f, h2, x, h1, x, 0, false, i0 + 4, 0)) return cleanup(s);
     }
+    p->runs.back().nops = static_cast<int>(ops.size()) - p->runs.back().op0;
+    p->runs.back().units = done;
     p->alg_bytes += p->weight_bytes;
     p->nops = static_cast<int>(ops.size());
-    // device image: [maps (64-B aligned)] [ops] [sync + counters] [partials]
+    // device image: [maps (64-B aligned)] [ops] [sync per run] [flags] [tickets x2] [partials x2]
+    auto up = [](size_t v) { return (v + 255) / 256 * 256; };
     const size_t maps_bytes = maps.size() * sizeof(CUtensorMap);
-    const size_t ops_off = (maps_bytes + 255) / 256 * 256;
+    const size_t ops_off = up(maps_bytes);
     const size_t ops_bytes = ops.size() * sizeof(hp::dstage_op);
-    const size_t sync_off = (ops_off + ops_bytes + 255) / 256 * 256;
-    const size_t sync_bytes = (2 + static_cast<size_t>(max_nt)) * sizeof(unsigned);
-    const size_t part_off = (sync_off + sync_bytes + 255) / 256 * 256;
-    auto* base = static_cast<char*>(dalloc(part_off + part_bytes));
+    const size_t sync_off = up(ops_off + ops_bytes);
+    const size_t sync_bytes = p->runs.size() * 256;
+    const size_t flags_off = up(sync_off + sync_bytes);
+    const size_t flags_bytes = static_cast<size_t>(nflags) * 4;
+    const size_t tick_off = up(flags_off + flags_bytes);
+    const size_t tick_bytes = up(static_cast<size_t>(max_nt) * 4);
+    const size_t part_off = up(tick_off + 2 * tick_bytes);
+    auto* base = static_cast<char*>(dalloc(part_off + 2 * part_bytes));
     if (!base) return cleanup(fail(HP_ECUDA, "decode_plan: cudaMalloc"));
     auto* dmaps = reinterpret_cast<CUtensorMap*>(base);
-    for (size_t i = 0; i < ops.size(); ++i)
+    auto* dflags = reinterpret_cast<unsigned*>(base + flags_off);
+    for (size_t i = 0; i < ops.size(); ++i) {
         if (map_of[i] >= 0) ops[i].tmap = dmaps + map_of[i];
+        if (ops[i].kind == 0 && flag_of[i].first >= 0) ops[i].out_flags = dflags + flag_of[i].first;
+    }
+    for (size_t i = 0; i < ops.size(); ++i) {  // dataflow edges: the producer's flags
+        if (ops[i].kind == 0 && flag_of[i].first < 0 && flag_of[i].second >= 0)
+            ops[i].dep_flags = ops[flag_of[i].second].out_flags;
+    }
+    for (size_t r = 0; r < p->runs.size(); ++r)
+        p->runs[r].sync = reinterpret_cast<unsigned long long*>(base + sync_off + r * 256);
     p->d_ops = reinterpret_cast<hp::dstage_op*>(base + ops_off);
-    p->sync = reinterpret_cast<unsigned*>(base + sync_off);
-    p->counters = p->sync + 2;
-    p->partial = reinterpret_cast<float*>(base + part_off);
+    for (int b = 0; b < 2; ++b) {
+        p->counters[b] = reinterpret_cast<unsigned*>(base + tick_off + b * tick_bytes);
+        p->partial[b] = reinterpret_cast<float*>(base + part_off + b * part_bytes);
+    }
     if (cudaMemcpy(dmaps, maps.data(), maps_bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(p->d_ops, ops.data(), ops_bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemset(p->sync, 0, sync_bytes) != cudaSuccess)
+        cudaMemset(base + sync_off, 0, part_off - sync_off) != cudaSuccess)
         return cleanup(fail(HP_ECUDA, "decode_plan: upload"));
     *out = p;
     return HP_OK;
@@ -482,11 +531,26 @@ hp_status hp_decode_plan_create(const hp_decoder_layer* layers, int n_layers, vo
 
 hp_status hp_decode_plan_run(hp_decode_plan* p, hp_stream stream) {
     if (!p) return fail(HP_EINVAL, "decode_plan_run: NULL plan");
-    int nops = p->nops;
-    if (const char* e = getenv("HP_DSTAGE_NOPS")) nops = std::min(nops, atoi(e));  // debug
-    return cuda_status(hp::launch_dstage(p->d_ops, nops, p->m, p->sym, p->sync, p->counters,
-                                         p->partial, p->grid, static_cast<cudaStream_t>(stream)),
-                       "decode_plan_run");
+    int limit = p->nops;
+    if (const char* e = getenv("HP_DSTAGE_NOPS")) limit = std::min(limit, atoi(e));  // debug
+    for (const auto& r : p->runs) {
+        const int n = std::min(r.nops, limit - r.op0);
+        if (n <= 0) break;
+        // a truncated run (debug) must still see its full per-launch unit count
+        // only when complete; recompute for the prefix
+        unsigned long long units = r.units;
+        if (n < r.nops) {
+            std::vector<hp::dstage_op> tmp(1);
+            cudaMemcpy(tmp.data(), p->d_ops + r.op0 + n, sizeof(hp::dstage_op), cudaMemcpyDeviceToHost);
+            units = tmp[0].wait;
+        }
+        if (hp_status s = cuda_status(
+                hp::launch_dstage(p->d_ops + r.op0, n, p->m, r.bits, p->sym, r.sync, units, p->counters,
+                                  p->partial, p->grid, static_cast<cudaStream_t>(stream)),
+                "decode_plan_run"))
+            return s;
+    }
+    return HP_OK;
 }
 
 hp_status hp_decode_plan_info(hp_decode_plan* p, double* out4) {

@@ -152,11 +152,10 @@ __global__ void __launch_bounds__(128)
             int q = 0;  // padding / invalid rows: signed code 0
             if (row_ok && kk < cnt) q = quant_code(__bfloat162float(tile[r][kk]), gg);
             const uint32_t sc = static_cast<uint32_t>(q + off);
-            const code_pos p = locate_code(BITS, kk);
             if constexpr (BITS == 3) {
-                words[p.chunk * 4 + p.word] |= (sc & 3u) << p.shift;
-                words[p.chunk2 * 4 + p.word2] |= ((sc >> 2) & 1u) << p.shift2;
+                put_code3(words, kk, sc);
             } else {
+                const code_pos p = locate_code(BITS, kk);
                 words[p.chunk * 4 + p.word] |= sc << p.shift;
             }
         }
@@ -194,13 +193,14 @@ __global__ void unpack_kernel(const uint8_t* __restrict__ packed,
             const uint16_t v = *reinterpret_cast<const uint16_t*>(base + (kk >> 3) * 2048 + (kk & 7) * 2);
             reinterpret_cast<uint16_t*>(codes)[row * k_in + k0 + kk] = v;
         } else {
-            const code_pos p = locate_code(BITS, kk);
-            const uint32_t* wd = reinterpret_cast<const uint32_t*>(base + p.chunk * 2048);
             uint32_t c;
             if constexpr (BITS == 3) {
-                const uint32_t* hd = reinterpret_cast<const uint32_t*>(base + p.chunk2 * 2048);
-                c = ((wd[p.word] >> p.shift) & 3u) | (((hd[p.word2] >> p.shift2) & 1u) << 2);
+                c = get_code3(reinterpret_cast<const uint32_t*>(base),
+                              reinterpret_cast<const uint32_t*>(base + 2048),
+                              reinterpret_cast<const uint32_t*>(base + 4096), kk);
             } else {
+                const code_pos p = locate_code(BITS, kk);
+                const uint32_t* wd = reinterpret_cast<const uint32_t*>(base + p.chunk * 2048);
                 c = (wd[p.word] >> p.shift) & ((1u << BITS) - 1u);
             }
             codes[row * k_in + k0 + kk] = static_cast<uint8_t>(c);

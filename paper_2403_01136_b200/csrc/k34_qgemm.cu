@@ -162,7 +162,7 @@ struct qgemm_cfg {
     static constexpr int NG = SPS >= 4 ? SPS / 4 : 1;            // groups touched per stage
     static constexpr int kB = BN * 64 * SPS;                     // SPS/2 64-k swizzled sub-tiles
     static constexpr int kCodes = SPS >= 4 ? BITS * 2048 * NG
-                                           : (BITS == 3 ? 4096 : BITS * 1024);  // half group
+                                           : (BITS == 3 ? 6144 : BITS * 1024);  // half group (3-bit: whole group)
     static constexpr int kScale = BITS == 16 ? 0 : 1024 * NG;    // NG scale rows + NG zero rows
     static constexpr int kCS = kCodes + kScale;                  // weight-ring slot
     // Two rings: the weight-code ring (HBM latency, released as soon as the
@@ -384,9 +384,10 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
                 } else {
                     const int h = (sl >> 1) & 1;  // which half of the group
                     if constexpr (BITS == 3) {
-                        // low-2-bit plane of this half + the whole bit-2 plane
-                        bulk_g2s_elect(stage_codes(s), gsrc + h * 2048, 2048, &full_c[s]);
-                        bulk_g2s_elect(stage_codes(s) + 2048, gsrc + 2 * 2048, 2048, &full_c[s]);
+                        // a slice's three words sit in all three chunks: the
+                        // half-group stage carries the whole group
+                        (void)h;
+                        bulk_g2s_elect(stage_codes(s), gsrc, 6144, &full_c[s]);
                     } else {
                         bulk_g2s_elect(stage_codes(s), gsrc + h * (BITS * 1024), BITS * 1024, &full_c[s]);
                     }
@@ -496,12 +497,8 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
                     if constexpr (SPS >= 4) {
                         load_slice<BITS>(cbase + (x >> 2) * (BITS * 2048), x & 3, wv[h]);
                     } else if constexpr (BITS == 3) {
-                        // half-group stage: lo plane at chunk 0, bit-2 plane at chunk 1
-                        const int gs = ((sl & 3) + x);  // slice index within the group
-                        const uint2 lo = lds64(cbase + 8 * (gs & 1));
-                        wv[h].w[0] = lo.x;
-                        wv[h].w[1] = lo.y;
-                        wv[h].w[2] = lds32(cbase + 2048 + 4 * gs);
+                        // half-group stage holding the whole group
+                        load_slice<BITS>(cbase, (sl & 3) + x, wv[h]);
                     } else {
                         load_slice<BITS>(cbase, x, wv[h]);
                     }

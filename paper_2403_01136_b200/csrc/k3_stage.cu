@@ -60,23 +60,45 @@ struct dstage_op {
     int64_t ln_ldx, ln_ldy;
     int h;
     int P;                    // CTAs the op is split over (= K3's grid for it)
+    // dataflow between consecutive GEMMs: this op's k-group g needs output
+    // tile dep_off + g of the producing op (its out_flags == epoch + 1)
+    const unsigned* dep_flags;
+    unsigned* out_flags;      // per output tile, set to epoch + 1 when written
+    int dep_off;
+    int pbuf;                 // stream-K workspace parity (consecutive GEMMs differ)
 };
 
-static_assert(sizeof(dstage_op) == 168, "dstage_op layout is shared by k3_stage.cu and capi.cu");
+static_assert(sizeof(dstage_op) == 192, "dstage_op layout is shared by k3_stage.cu and capi.cu");
 struct dstage_args {
     const dstage_op* ops;
     int nops;
     int m;
-    unsigned* sync;      // [0] done, [1] exit ticket
-    unsigned* counters;  // per-tile stream-K tickets
-    float* partial;      // [tiles][maxseg][BN/4][128] float4
+    unsigned long long* sync;   // [0] done (u64, never reset), [1] = {epoch u32, exit ticket u32}
+    unsigned long long units;   // units (tiles + LN rows) per launch: done target base = epoch * units
+    unsigned* counters[2];      // per-tile stream-K tickets, per parity
+    float* partial[2];          // [tiles][maxseg][BN/4][128] float4, per parity
+    unsigned long long* trace;  // HP_DSTAGE_TRACE builds: [cta][op][4] globaltimer
 };
+
+// Debug trace (HP_DSTAGE_TRACE): per CTA and op, the %globaltimer when
+// 0: the activation producer saw the op's inputs complete, 1: the epilogue
+// finished the op, 2: dequant warp 4 finished the op's stages, 3: the
+// weight producer issued the op's last stage.
+__device__ __forceinline__ void dtrace(const dstage_args& a, int oi, int ev) {
+#ifdef HP_DSTAGE_TRACE
+    if (a.trace && oi < 256) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.trace[(static_cast<size_t>(blockIdx.x) * 256 + oi) * 8 + ev] = t;
+    }
+#endif
+}
 
 namespace {
 
 constexpr int kBN = 32;
 #ifndef HP_DSTAGE_DWG
-#define HP_DSTAGE_DWG 2
+#define HP_DSTAGE_DWG 3
 #endif
 constexpr int kDWG = HP_DSTAGE_DWG;     // dequant warpgroups, stages round-robin
 constexpr int kThreads = 128 * (2 + kDWG);
@@ -90,6 +112,8 @@ constexpr int kA0 = 64;                 // TMEM: 2 accumulators of 32 cols, then
 constexpr int kACols = 128;             // up to 8 slices x 16 cols
 constexpr int kAS = (448 / kACols) / kDWG * kDWG;  // TMEM A stages, a multiple of kDWG
 constexpr int kStgLd = 132;
+constexpr int kHB = 4;    // epilogue -> reducer handoffs in flight (named barriers kHB0..)
+constexpr int kHB0 = 4;
 
 template <bool SYM>
 struct dcfg {
@@ -131,22 +155,53 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_release64(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
 __device__ __forceinline__ void fence_proxy_async_global() {
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
-__device__ __forceinline__ void wait_done(const unsigned* done, unsigned target) {
+__device__ __forceinline__ void wait_done(const unsigned long long* done, unsigned long long target) {
 #ifdef HP_DSTAGE_WATCHDOG
     long long n = 0;
-    while (ld_acquire(done) < target) {
-        __nanosleep(40);
+    while (ld_acquire64(done) < target) {
+        __nanosleep(32);
         if (++n == (1ll << 22)) {
-            printf("dstage hang: cta %d warp %d wait_done %u (have %u)\n", blockIdx.x, threadIdx.x / 32, target,
-                   ld_acquire(done));
+            printf("dstage hang: cta %d warp %d wait_done %llu (have %llu)\n", blockIdx.x, threadIdx.x / 32,
+                   target, ld_acquire64(done));
             __trap();
         }
     }
 #else
-    while (ld_acquire(done) < target) __nanosleep(40);
+    while (ld_acquire64(done) < target) __nanosleep(32);
+#endif
+}
+__device__ __forceinline__ void wait_flag(const unsigned* f, unsigned v) {
+#ifdef HP_DSTAGE_WATCHDOG
+    long long n = 0;
+    while (ld_acquire(f) != v) {
+        __nanosleep(32);
+        if (++n == (1ll << 22)) {
+            printf("dstage hang: cta %d warp %d flag want %u have %u\n", blockIdx.x, threadIdx.x / 32, v,
+                   ld_acquire(f));
+            __trap();
+        }
+    }
+#else
+    while (ld_acquire(f) != v) __nanosleep(32);
 #endif
 }
 
@@ -261,12 +316,17 @@ __device__ __forceinline__ void store16(const dstage_op& op, int m, float* stg, 
     asm volatile("bar.sync 2, 128;" ::: "memory");
 }
 
-// The 128 epilogue threads publish `units` finished units of work.
-__device__ __forceinline__ void publish(unsigned* done, unsigned units) {
-    __threadfence();
-    fence_proxy_async_global();
+// The 128 epilogue threads publish one finished unit: bar.sync orders every
+// thread's stores before thread 0's gpu-scope release (cumulative), the
+// pattern of CUTLASS's split-K semaphore; one release instead of 128 full
+// fences (a fence.sc per thread cost ~1.8 us on the critical path).
+__device__ __forceinline__ void publish(unsigned long long* done, unsigned* flag, unsigned epoch1) {
     asm volatile("bar.sync 1, 128;" ::: "memory");
-    if ((threadIdx.x & 127) == 0) atomicAdd(done, units);
+    if ((threadIdx.x & 127) == 0) {
+        fence_proxy_async_global();  // consumers read these outputs with TMA
+        if (flag) st_release(flag, epoch1);
+        red_release64(done, 1ull);
+    }
 }
 
 // LayerNorm of row `row` by the 128 epilogue threads, bit-identical to
@@ -277,7 +337,7 @@ __device__ __forceinline__ void publish(unsigned* done, unsigned units) {
 // thread), else are re-read from L2 (same values, same order).
 template <bool CACHED>
 __device__ __forceinline__ void ln_row(const dstage_op& op, int row, float* red) {
-    constexpr int MAXV = CACHED ? 4 : 1;  // cached: h <= 8192 (nv <= 1024)
+    constexpr int MAXV = CACHED ? 3 : 1;  // cached: h <= 6144 (nv <= 768)
     const int t = threadIdx.x & 127;
     const int lane = t & 31, wq = t >> 5;
     const uint4* xr = reinterpret_cast<const uint4*>(op.ln_x + row * op.ln_ldx);
@@ -432,41 +492,17 @@ __device__ __forceinline__ void dq_stage(uint32_t slot, int r, int nsl, uint32_t
     }
 }
 
-// All stages of one GEMM op for one dequant warp (round-robin over the
-// kDWG warpgroups by the global stage counter `it`).
-template <int BITS, bool SYM, int SPS, int CR>
-__device__ __forceinline__ void dq_op(const dstage_op& op, uint32_t& it_io, int wg, int r,
-                                   uint32_t tmem_lane, int lane, uint64_t* full_c,
-                                   uint64_t* empty_c, uint64_t* afull, uint64_t* aempty,
-                                   uint32_t codes0) {
-    constexpr int kCS = dcfg<SYM>::kCS;
-    uint32_t it = it_io;
-    seg_iter iter;
-    iter.init(op.total, op.G, op.P);
-    seg_t sg;
-    while (iter.next(sg)) {
-        for (int sl = 4 * sg.g0; sl < 4 * sg.g1; sl += SPS, ++it) {
-            if (static_cast<int>(it % kDWG) != wg) continue;
-            const int nsl = min(SPS, 4 * sg.g1 - sl);
-            const int s = it % CR, as = it % kAS;
-            MBW(&full_c[s], (it / CR) & 1, 1);
-            MBW(&aempty[as], ((it / kAS) & 1) ^ 1, 2);
-            tc_fence_after();
-            dq_stage<BITS, SYM, SPS>(codes0 + s * kCS, r, nsl, tmem_lane + kA0 + as * kACols, &empty_c[s],
-                                     lane);
-            tmem_st_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&afull[as]);
-        }
-    }
-    it_io = it;
-}
+template <int BITS>
+constexpr int kSPS = BITS <= 4 ? 8 : (BITS == 8 ? 4 : 2);  // 32-k slices per stage
 
-template <bool SYM>
+// One launch runs every op of a run of layers with the same bit width (the
+// dequant code is then one instantiation: a runtime bit switch spilled).
+template <int BITS, bool SYM>
 __global__ void __launch_bounds__(kThreads, 1) dstage_kernel(const dstage_args a) {
     using C = dcfg<SYM>;
     constexpr int CR = C::CR;
+    constexpr int SPS = kSPS<BITS>;
+    constexpr int NGMAX = SPS >= 4 ? SPS / 4 : 1;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -482,13 +518,22 @@ __global__ void __launch_bounds__(kThreads, 1) dstage_kernel(const dstage_args a
     uint64_t* aempty = afull + kAS;
     uint64_t* tfull = aempty + kAS;
     uint64_t* tempty = tfull + kNACC;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kNACC);
+    uint64_t* hfree = tempty + kNACC;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hfree + kHB);
     unsigned* bcast = tmem_slot + 1;
     float* red = reinterpret_cast<float*>(bcast + 2);  // 8 floats
+    unsigned* tres = reinterpret_cast<unsigned*>(red + 8);           // ticket results ring (8)
+    volatile unsigned* tcount = reinterpret_cast<volatile unsigned*>(tres + 8);  // results posted
 
     const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
     const int lane = threadIdx.x & 31;
-    unsigned* done = a.sync;
+    unsigned long long* done = a.sync;
+    unsigned* epoch_exit = reinterpret_cast<unsigned*>(a.sync + 1);
+    // stable for the whole launch: only the last CTA of the PREVIOUS launch
+    // advanced it
+    const unsigned epoch = __ldcg(epoch_exit);
+    const unsigned epoch1 = epoch + 1u;
+    const unsigned long long base = static_cast<unsigned long long>(epoch) * a.units;
 
     if (warp == 1 && lane == 0) {
         for (int i = 0; i < CR; ++i) {
@@ -507,6 +552,8 @@ __global__ void __launch_bounds__(kThreads, 1) dstage_kernel(const dstage_args a
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 4);
         }
+        for (int i = 0; i < kHB; ++i) mbar_init(&hfree[i], 1);
+        *tcount = 0u;
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
@@ -522,56 +569,71 @@ __global__ void __launch_bounds__(kThreads, 1) dstage_kernel(const dstage_args a
         for (int oi = 0; oi < a.nops; ++oi) {
             const dstage_op& op = a.ops[oi];
             if (op.kind != 0) continue;
-            const int bits = op.bits, sps = op.sps, ngmax = sps >= 4 ? sps / 4 : 1;
+            const uint8_t* packed = op.packed;
+            const float* scale = op.scale;
+            const float* zero = op.zero;
+            const int G = op.G;
             seg_iter iter;
-            iter.init(op.total, op.G, op.P);
+            iter.init(op.total, G, op.P);
             while (iter.next(sg)) {
-                const int nt = sg.tile;
-                for (int sl = 4 * sg.g0; sl < 4 * sg.g1; sl += sps, ++it) {
+                for (int sl = 4 * sg.g0; sl < 4 * sg.g1; sl += SPS, ++it) {
                     const int g = sl >> 2;
-                    const int ng = sps >= 4 ? min(ngmax, sg.g1 - g) : 1;
+                    const int ng = SPS >= 4 ? min(NGMAX, sg.g1 - g) : 1;
                     const int s = it % CR;
                     MBWW(&empty_c[s], ((it / CR) & 1) ^ 1, 3);
-                    const size_t t = static_cast<size_t>(nt) * op.G + g;
-                    const uint8_t* gsrc = op.packed + t * (bits * 2048);
+                    const size_t t = static_cast<size_t>(sg.tile) * G + g;
+                    const uint8_t* gsrc = packed + t * (BITS * 2048);
                     uint32_t cbytes, coff = 0;
-                    if (sps >= 4) {
-                        cbytes = static_cast<uint32_t>(ng) * bits * 2048;
+                    if constexpr (SPS >= 4) {
+                        cbytes = static_cast<uint32_t>(ng) * BITS * 2048;
                     } else {  // 16-bit half group
                         cbytes = 16384;
                         coff = ((sl >> 1) & 1) * 16384;
                     }
-                    const uint32_t sbytes = bits == 16 ? 0u : static_cast<uint32_t>(ng) * 512u * (SYM ? 1 : 2);
+                    const uint32_t sbytes = BITS == 16 ? 0u : static_cast<uint32_t>(ng) * 512u * (SYM ? 1 : 2);
                     mbar_arrive_expect_tx_elect(&full_c[s], cbytes + sbytes);
                     bulk_g2s_elect(stage_codes(s), gsrc + coff, cbytes, &full_c[s]);
-                    if (bits != 16) {
-                        bulk_g2s_elect(stage_codes(s) + kCodeBytes, op.scale + t * 128, ng * 512u, &full_c[s]);
-                        if (!SYM)
-                            bulk_g2s_elect(stage_codes(s) + kCodeBytes + 1024, op.zero + t * 128, ng * 512u,
+                    if constexpr (BITS != 16) {
+                        bulk_g2s_elect(stage_codes(s) + kCodeBytes, scale + t * 128, ng * 512u, &full_c[s]);
+                        if constexpr (!SYM)
+                            bulk_g2s_elect(stage_codes(s) + kCodeBytes + 1024, zero + t * 128, ng * 512u,
                                            &full_c[s]);
                     }
                 }
             }
+            if (lane == 0) dtrace(a, oi, 3);
         }
     } else if (warp == 3) {
-        // ============ activation producer: waits for the op's input ============
+        // ============ activation producer: waits for the op's inputs ===========
         uint32_t it = 0;
         for (int oi = 0; oi < a.nops; ++oi) {
             const dstage_op& op = a.ops[oi];
             if (op.kind != 0) continue;
-            const int sps = op.sps;
-            if (lane == 0) wait_done(done, op.wait);
-            __syncwarp();
-            fence_proxy_async_global();
-            const uint32_t bytes = static_cast<uint32_t>(kBN * 128 * (sps / 2));
+            const CUtensorMap* tmap = op.tmap;
+            const unsigned* dep = op.dep_flags;
+            const int dep_off = op.dep_off;
+            if (!dep) {  // input written by a LayerNorm (or before the launch)
+                if (lane == 0) wait_done(done, base + op.wait);
+                __syncwarp();
+                fence_proxy_async_global();
+            }
+            if (lane == 0) dtrace(a, oi, 0);
+            constexpr uint32_t bytes = static_cast<uint32_t>(kBN * 128 * (SPS / 2));
             seg_iter iter;
             iter.init(op.total, op.G, op.P);
             while (iter.next(sg)) {
-                for (int sl = 4 * sg.g0; sl < 4 * sg.g1; sl += sps, ++it) {
+                for (int sl = 4 * sg.g0; sl < 4 * sg.g1; sl += SPS, ++it) {
                     const int s = it % kBR;
                     MBWW(&empty_b[s], ((it / kBR) & 1) ^ 1, 4);
+                    if (dep) {  // dataflow: only the producer tiles this stage reads
+                        const int g = sl >> 2;
+                        const int ng = SPS >= 4 ? min(NGMAX, sg.g1 - g) : 1;
+                        if (lane < ng) wait_flag(dep + dep_off + g + lane, epoch1);
+                        __syncwarp();
+                        fence_proxy_async_global();
+                    }
                     mbar_arrive_expect_tx_elect(&full_b[s], bytes);
-                    tma_load_3d_elect(stage_b(s), op.tmap, 0, 0, sl >> 1, &full_b[s]);
+                    tma_load_3d_elect(stage_b(s), tmap, 0, 0, sl >> 1, &full_b[s]);
                 }
             }
         }
@@ -582,7 +644,6 @@ __global__ void __launch_bounds__(kThreads, 1) dstage_kernel(const dstage_args a
         for (int oi = 0; oi < a.nops; ++oi) {
             const dstage_op& op = a.ops[oi];
             if (op.kind != 0) continue;
-            const int sps = op.sps;
             seg_iter iter;
             iter.init(op.total, op.G, op.P);
             while (iter.next(sg)) {
@@ -590,8 +651,8 @@ __global__ void __launch_bounds__(kThreads, 1) dstage_kernel(const dstage_args a
                 MBWW(&tempty[acc], ((ut / kNACC) & 1) ^ 1, 5);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem + acc * kBN;
-                for (int sl = 4 * sg.g0; sl < 4 * sg.g1; sl += sps, ++it) {
-                    const int nsl = min(sps, 4 * sg.g1 - sl);
+                for (int sl = 4 * sg.g0; sl < 4 * sg.g1; sl += SPS, ++it) {
+                    const int nsl = min(SPS, 4 * sg.g1 - sl);
                     const int s = it % kBR, as = it % kAS;
                     MBWW(&full_b[s], (it / kBR) & 1, 6);
                     MBWW(&afull[as], (it / kAS) & 1, 7);
@@ -599,7 +660,7 @@ __global__ void __launch_bounds__(kThreads, 1) dstage_kernel(const dstage_args a
                     const uint64_t bdesc0 = umma_desc_sw128(smem_u32(stage_b(s)));
                     const uint32_t abase = tmem + kA0 + as * kACols;
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
+                    for (int q = 0; q < SPS / 2; ++q) {
                         if (2 * q < nsl)
                             mma_ts_x4_elect(d_tmem, abase + q * 32, bdesc0 + q * (kBN * 8), idesc,
                                             (sl > 4 * sg.g0 || q > 0) ? 1u : 0u);
@@ -617,18 +678,91 @@ __global__ void __launch_bounds__(kThreads, 1) dstage_kernel(const dstage_args a
         const int lq = warp & 3;
         const int wg = q >> 2;
         const int r = lq * 32 + lane;
-        const uint32_t lane_addr = static_cast<uint32_t>(lq * 32) << 16;
+        const uint32_t tmem_lane = tmem + (static_cast<uint32_t>(lq * 32) << 16);
+        const uint32_t codes0 = smem_u32(stage_codes(0));
         uint32_t it = 0;
         for (int oi = 0; oi < a.nops; ++oi) {
             const dstage_op& op = a.ops[oi];
             if (op.kind != 0) continue;
-            // one loop per bit width: each instantiation gets its own
-            // register allocation (a per-stage switch spilled)
-            switch (op.bits) {
-                case 3: dq_op<3, SYM, 8, CR>(op, it, wg, r, tmem + lane_addr, lane, full_c, empty_c, afull, aempty, smem_u32(stage_codes(0))); break;
-                case 4: dq_op<4, SYM, 8, CR>(op, it, wg, r, tmem + lane_addr, lane, full_c, empty_c, afull, aempty, smem_u32(stage_codes(0))); break;
-                case 8: dq_op<8, SYM, 4, CR>(op, it, wg, r, tmem + lane_addr, lane, full_c, empty_c, afull, aempty, smem_u32(stage_codes(0))); break;
-                default: dq_op<16, SYM, 2, CR>(op, it, wg, r, tmem + lane_addr, lane, full_c, empty_c, afull, aempty, smem_u32(stage_codes(0))); break;
+            seg_iter iter;
+            iter.init(op.total, op.G, op.P);
+            while (iter.next(sg)) {
+                for (int sl = 4 * sg.g0; sl < 4 * sg.g1; sl += SPS, ++it) {
+                    if (static_cast<int>(it % kDWG) != wg) continue;
+                    const int nsl = min(SPS, 4 * sg.g1 - sl);
+                    const int s = it % CR, as = it % kAS;
+                    MBW(&full_c[s], (it / CR) & 1, 1);
+                    MBW(&aempty[as], ((it / kAS) & 1) ^ 1, 2);
+                    tc_fence_after();
+                    dq_stage<BITS, SYM, SPS>(codes0 + s * C::kCS, r, nsl, tmem_lane + kA0 + as * kACols,
+                                             &empty_c[s], lane);
+                    tmem_st_wait();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&afull[as]);
+                }
+            }
+            if (warp == 4 && lane == 0) dtrace(a, oi, 2);
+        }
+    } else if (warp == 2) {
+        // ===================== publisher (release latency off the epilogue) ====
+        // A gpu-scope release (publishing a tile) or the acq_rel ticket of a
+        // split tile waits ~2 us for the stores before it to be acknowledged
+        // while the weight stream loads L2. This warp absorbs those waits:
+        // the epilogue hands each finished segment over through a named
+        // barrier (bar.arrive there / bar.sync here orders its stores before
+        // our release) and goes on. Split tiles: we take the ticket and post
+        // the result; the epilogue reduces the tiles it won at the end of the
+        // op (128 threads) and hands them back for publishing.
+        uint32_t ht = 0, nres = 0;
+        for (int oi = 0; oi < a.nops; ++oi) {
+            const dstage_op& op = a.ops[oi];
+            if (op.kind != 0) continue;
+            unsigned* counters = a.counters[op.pbuf];
+            unsigned* oflags = op.out_flags;
+            int won0 = -1, won1 = -1;
+            seg_iter iter;
+            iter.init(op.total, op.G, op.P);
+            while (iter.next(sg)) {
+                const int hb = ht % kHB;
+                asm volatile("bar.sync %0, 160;" ::"r"(kHB0 + hb) : "memory");
+                if (lane == 0) mbar_arrive(&hfree[hb]);
+                ++ht;
+                if (sg.nseg == 1) {
+                    if (lane == 0) {
+                        fence_proxy_async_global();
+                        if (oflags) st_release(oflags + sg.tile, epoch1);
+                        red_release64(done, 1ull);
+                    }
+                } else {
+                    if (lane == 0) {
+                        const unsigned t = atom_add_acq_rel(&counters[sg.tile], 1u);
+                        const bool last = t == static_cast<unsigned>(sg.nseg - 1);
+                        if (last) counters[sg.tile] = 0u;  // nobody else touches it this op
+                        tres[nres % 8] = last ? 1u : 0u;
+                        __threadfence_block();
+                        *tcount = nres + 1;
+                    }
+                    const bool last = __shfl_sync(0xffffffffu, lane == 0 ? tres[nres % 8] : 0u, 0) != 0u;
+                    ++nres;
+                    if (last) {
+                        if (won0 < 0) won0 = sg.tile; else won1 = sg.tile;
+                    }
+                }
+            }
+            // tiles this CTA reduces: publish once the epilogue stored them
+            for (int j = 0; j < 2; ++j) {
+                const int tile = j == 0 ? won0 : won1;
+                if (tile < 0) continue;
+                const int hb = ht % kHB;
+                asm volatile("bar.sync %0, 160;" ::"r"(kHB0 + hb) : "memory");
+                if (lane == 0) {
+                    mbar_arrive(&hfree[hb]);
+                    fence_proxy_async_global();
+                    if (oflags) st_release(oflags + tile, epoch1);
+                    red_release64(done, 1ull);
+                }
+                ++ht;
             }
         }
     } else if (warp >= kEpiWarp0) {
@@ -637,21 +771,30 @@ __global__ void __launch_bounds__(kThreads, 1) dstage_kernel(const dstage_args a
         const int r = lq * 32 + lane;
         const uint32_t lane_addr = static_cast<uint32_t>(lq * 32) << 16;
         const int tid = threadIdx.x & 127;
-        uint32_t ut = 0;
+        uint32_t ut = 0, ht = 0, nres = 0;
+        auto handoff = [&]() {
+            const int hb = ht % kHB;
+            MBW(&hfree[hb], ((ht / kHB) & 1) ^ 1, 9);
+            asm volatile("bar.arrive %0, 160;" ::"r"(kHB0 + hb) : "memory");
+            ++ht;
+        };
         for (int oi = 0; oi < a.nops; ++oi) {
             const dstage_op& op = a.ops[oi];
             if (op.kind == 1) {
                 if (static_cast<int>(blockIdx.x) < a.m) {
-                    if (tid == 0) wait_done(done, op.wait);
+                    if (tid == 0) wait_done(done, base + op.wait);
                     asm volatile("bar.sync 1, 128;" ::: "memory");
-                    if (op.h <= 8192)
+                    if (op.h <= 6144)
                         ln_row<true>(op, blockIdx.x, red);
                     else
                         ln_row<false>(op, blockIdx.x, red);
-                    publish(done, 1u);
+                    publish(done, nullptr, epoch1);
+                    if (tid == 0) dtrace(a, oi, 1);
                 }
                 continue;
             }
+            float* partial = a.partial[op.pbuf];
+            int split_tile[2] = {-1, -1}, split_nseg[2] = {0, 0}, nsplit = 0;
             seg_iter iter;
             iter.init(op.total, op.G, op.P);
             while (iter.next(sg)) {
@@ -660,7 +803,7 @@ __global__ void __launch_bounds__(kThreads, 1) dstage_kernel(const dstage_args a
                 MBW(&tfull[acc], (ut / kNACC) & 1, 8);
                 tc_fence_after();
                 float4* part = sg.nseg > 1
-                                   ? reinterpret_cast<float4*>(a.partial) +
+                                   ? reinterpret_cast<float4*>(partial) +
                                          (static_cast<size_t>(sg.tile) * op.maxseg + sg.idx) * (kBN / 4) * 128 + r
                                    : nullptr;
 #pragma unroll 1
@@ -684,58 +827,68 @@ __global__ void __launch_bounds__(kThreads, 1) dstage_kernel(const dstage_args a
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tempty[acc]);
-                if (sg.nseg == 1) {
-                    publish(done, 1u);
-                } else {
-                    __threadfence();
-                    asm volatile("bar.sync 1, 128;" ::: "memory");
-                    if (tid == 0) *bcast = atomicAdd(&a.counters[sg.tile], 1u);
-                    asm volatile("bar.sync 1, 128;" ::: "memory");
-                    if (*bcast == static_cast<unsigned>(sg.nseg - 1)) {
-                        __threadfence();
-                        constexpr int kRB = 2;
-                        const float4* base = reinterpret_cast<const float4*>(a.partial) +
-                                             static_cast<size_t>(sg.tile) * op.maxseg * (kBN / 4) * 128 + r;
-#pragma unroll 1
-                        for (int c = 0; c < kBN / 16; ++c) {
-                            const int c0 = 16 * c;
-                            float f[16];
-#pragma unroll
-                            for (int i = 0; i < 16; ++i) f[i] = 0.f;
-#pragma unroll 1
-                            for (int jb = 0; jb < sg.nseg; jb += kRB) {
-                                float4 q4[kRB][4];
-#pragma unroll
-                                for (int jj = 0; jj < kRB; ++jj) {
-                                    if (jb + jj < sg.nseg) {
-                                        const float4* src =
-                                            base + (static_cast<size_t>(jb + jj) * (kBN / 4) + c0 / 4) * 128;
-#pragma unroll
-                                        for (int i = 0; i < 4; ++i) q4[jj][i] = __ldcg(src + i * 128);
-                                    }
-                                }
-#pragma unroll
-                                for (int jj = 0; jj < kRB; ++jj) {
-                                    if (jb + jj < sg.nseg) {
-#pragma unroll
-                                        for (int i = 0; i < 4; ++i) {
-                                            f[4 * i] += q4[jj][i].x;
-                                            f[4 * i + 1] += q4[jj][i].y;
-                                            f[4 * i + 2] += q4[jj][i].z;
-                                            f[4 * i + 3] += q4[jj][i].w;
-                                        }
-                                    }
-                                }
-                            }
-                            store16(op, a.m, stg, r, f, c0, nt * 128);
-                        }
-                        if (tid == 0) a.counters[sg.tile] = 0u;
-                        publish(done, 1u);
-                    }
-                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                handoff();
+                if (sg.nseg > 1 && nsplit < 2) {
+                    split_tile[nsplit] = sg.tile;
+                    split_nseg[nsplit] = sg.nseg;
+                    ++nsplit;
                 }
                 ++ut;
             }
+            // split tiles: reduce the ones whose ticket we won (ordered sum of
+            // the segments' partials, K3's reducer arithmetic)
+            for (int j = 0; j < nsplit; ++j) {
+                if (tid == 0) {
+                    while (*tcount <= nres) {
+                    }
+                    __threadfence_block();
+                    *bcast = tres[nres % 8];
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                }
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                const bool won = *bcast != 0u;
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                ++nres;
+                if (!won) continue;
+                const int tile = split_tile[j], nseg = split_nseg[j];
+                constexpr int kRB = 2;
+                const float4* basep = reinterpret_cast<const float4*>(partial) +
+                                      static_cast<size_t>(tile) * op.maxseg * (kBN / 4) * 128 + r;
+#pragma unroll 1
+                for (int c = 0; c < kBN / 16; ++c) {
+                    const int c0 = 16 * c;
+                    float f[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) f[i] = 0.f;
+#pragma unroll 1
+                    for (int jb = 0; jb < nseg; jb += kRB) {
+                        float4 q4[kRB][4];
+#pragma unroll
+                        for (int jj = 0; jj < kRB; ++jj) {
+                            if (jb + jj < nseg) {
+                                const float4* src = basep + (static_cast<size_t>(jb + jj) * (kBN / 4) + c0 / 4) * 128;
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) q4[jj][i] = __ldcg(src + i * 128);
+                            }
+                        }
+#pragma unroll
+                        for (int jj = 0; jj < kRB; ++jj) {
+                            if (jb + jj < nseg) {
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) {
+                                    f[4 * i] += q4[jj][i].x;
+                                    f[4 * i + 1] += q4[jj][i].y;
+                                    f[4 * i + 2] += q4[jj][i].z;
+                                    f[4 * i + 3] += q4[jj][i].w;
+                                }
+                            }
+                        }
+                    }
+                    store16(op, a.m, stg, r, f, c0, tile * 128);
+                }
+                handoff();
+            }
+            if (tid == 0) dtrace(a, oi, 1);
         }
     }
 
@@ -746,17 +899,21 @@ __global__ void __launch_bounds__(kThreads, 1) dstage_kernel(const dstage_args a
     }
     if (threadIdx.x == 0) {
         __threadfence();
-        if (atomicAdd(&a.sync[1], 1u) == gridDim.x - 1) {
-            a.sync[0] = 0u;
-            a.sync[1] = 0u;
+        if (atomicAdd(epoch_exit + 1, 1u) == gridDim.x - 1) {
+            epoch_exit[1] = 0u;
             __threadfence();
+            st_release(epoch_exit, epoch1);
         }
     }
 }
 
 int g_dstage_sms = 0;
+unsigned long long* g_dstage_trace = nullptr;
 
 }  // namespace
+
+/* debug: copy the HP_DSTAGE_TRACE buffer ([148][256][4] u64) */
+extern "C" int hp_debug_dstage_trace(unsigned long long* host, int n);
 
 int dstage_grid() {
     if (g_dstage_sms == 0) {
@@ -769,40 +926,58 @@ int dstage_grid() {
     return (budget > 0 && budget < g_dstage_sms) ? budget : g_dstage_sms;
 }
 
-cudaError_t launch_dstage(const dstage_op* ops, int nops, int m, bool sym, unsigned* sync,
-                          unsigned* counters, float* partial, int grid, cudaStream_t st) {
-    dstage_args a{ops, nops, m, sync, counters, partial};
+template <int BITS, bool SYM>
+cudaError_t launch_dstage_t(const dstage_args& a, int grid, cudaStream_t st) {
+    static bool attr_done = false;
+    constexpr int smem = dcfg<SYM>::kSmem;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(dstage_kernel<BITS, SYM>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (they wait on each other)
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (sym) {
-        static bool done_attr = false;
-        cfg.dynamicSmemBytes = dcfg<true>::kSmem;
-        if (!done_attr) {
-            cudaError_t e = cudaFuncSetAttribute(dstage_kernel<true>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 dcfg<true>::kSmem);
-            if (e != cudaSuccess) return e;
-            done_attr = true;
-        }
-        return cudaLaunchKernelEx(&cfg, dstage_kernel<true>, a);
+    return cudaLaunchKernelEx(&cfg, dstage_kernel<BITS, SYM>, a);
+}
+
+// One launch = one run of consecutive layers with the same bit width.
+cudaError_t launch_dstage(const dstage_op* ops, int nops, int m, int bits, bool sym,
+                          unsigned long long* sync, unsigned long long units, unsigned* const counters[2],
+                          float* const partial[2], int grid, cudaStream_t st) {
+#ifdef HP_DSTAGE_TRACE
+    if (!g_dstage_trace) {
+        cudaMalloc(&g_dstage_trace, sizeof(unsigned long long) * 148 * 256 * 8);
+        cudaMemset(g_dstage_trace, 0, sizeof(unsigned long long) * 148 * 256 * 8);
     }
-    static bool done_attr = false;
-    cfg.dynamicSmemBytes = dcfg<false>::kSmem;
-    if (!done_attr) {
-        cudaError_t e = cudaFuncSetAttribute(dstage_kernel<false>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             dcfg<false>::kSmem);
-        if (e != cudaSuccess) return e;
-        done_attr = true;
+#endif
+    dstage_args a{ops, nops, m, sync, units, {counters[0], counters[1]}, {partial[0], partial[1]}, g_dstage_trace};
+    switch (bits * 2 + (sym ? 1 : 0)) {
+        case 7: return launch_dstage_t<3, true>(a, grid, st);
+        case 6: return launch_dstage_t<3, false>(a, grid, st);
+        case 9: return launch_dstage_t<4, true>(a, grid, st);
+        case 8: return launch_dstage_t<4, false>(a, grid, st);
+        case 17: return launch_dstage_t<8, true>(a, grid, st);
+        case 16: return launch_dstage_t<8, false>(a, grid, st);
+        case 33: return launch_dstage_t<16, true>(a, grid, st);
+        case 32: return launch_dstage_t<16, false>(a, grid, st);
     }
-    return cudaLaunchKernelEx(&cfg, dstage_kernel<false>, a);
+    return cudaErrorInvalidValue;
 }
 
 }  // namespace hp
+
+extern "C" int hp_debug_dstage_trace(unsigned long long* host, int n) {
+    if (!hp::g_dstage_trace) return 0;
+    cudaDeviceSynchronize();
+    cudaMemcpy(host, hp::g_dstage_trace, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost);
+    return n;
+}

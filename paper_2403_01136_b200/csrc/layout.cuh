@@ -16,10 +16,13 @@
 //   4-bit: chunk c covers kk in [32c, 32c+32); word j covers [32c+8j, +8);
 //          pair p<4 (kk0 = 32c+8j+2p): bits [4p,4p+4) = code(kk0),
 //          bits [16+4p, 20+4p) = code(kk0+1).
-//   3-bit: chunks 0/1 = low-2-bit planes of kk in [0,64) / [64,128):
-//          word j covers 16 kk; pair p<8: bits [2p,2p+2) and [16+2p,18+2p).
-//          chunk 2 = bit-2 plane: word j covers kk in [32j, 32j+32);
-//          pair p<16: bit p = code(kk0) bit 2, bit 16+p = code(kk0+1) bit 2.
+//   3-bit: slice s (kk in [32s, 32s+32)) owns word s of all three chunks
+//          (A = chunk 0, B = chunk 1, C = chunk 2). Pair i < 15 (kk0 =
+//          32s + 2i) is whole in word i/5, p = i%5: bits [3p, 3p+3) =
+//          code(kk0), bits [16+3p, 19+3p) = code(kk0+1), so one shift + one
+//          LOP3 per pair (the bit-plane layout needed two of each). Pair 15
+//          uses the spare bits: bit b of code(32s+30) at bit 15 of chunk b,
+//          bit b of code(32s+31) at bit 31 of chunk b.
 //   8-bit: chunk c covers [16c, 16c+16); word j covers [16c+4j, +4),
 //          byte i = code(kk0+i).
 //   16-bit: chunk c covers [8c, 8c+8) as bf16 in natural order.
@@ -68,14 +71,44 @@ __host__ __device__ __forceinline__ code_pos locate_code(int bits, int kk) {
         p.word = (kk >> 2) & 3;
         p.shift = 8 * (kk & 3);
     } else if (bits == 3) {
-        p.chunk = kk >> 6;
-        p.word = (kk >> 4) & 3;
-        p.shift = 2 * (pair & 7) + 16 * hi;
-        p.chunk2 = 2;
-        p.word2 = kk >> 5;
-        p.shift2 = (pair & 15) + 16 * hi;
+        // pairs 0..14: whole code at (chunk, word, shift); pair 15: bit b of
+        // the code at (chunk b, word, 15 + 16 hi) -- chunk2 = -1 marks it
+        const int i = pair & 15;
+        p.word = kk >> 5;
+        if (i < 15) {
+            p.chunk = i / 5;
+            p.shift = 3 * (i % 5) + 16 * hi;
+            p.chunk2 = 0;
+        } else {
+            p.chunk = 0;
+            p.shift = 15 + 16 * hi;
+            p.chunk2 = -1;
+        }
+        p.word2 = p.word;
+        p.shift2 = p.shift;
     }
     return p;
+}
+
+// 3-bit code kk of a row: write (into the row's 12 words, chunk-major) and read.
+__host__ __device__ __forceinline__ void put_code3(uint32_t* words, int kk, uint32_t sc) {
+    const code_pos p = locate_code(3, kk);
+    if (p.chunk2 == 0) {
+        words[p.chunk * 4 + p.word] |= (sc & 7u) << p.shift;
+    } else {
+#pragma unroll
+        for (int b = 0; b < 3; ++b) words[b * 4 + p.word] |= ((sc >> b) & 1u) << p.shift;
+    }
+}
+__host__ __device__ __forceinline__ uint32_t get_code3(const uint32_t* c0, const uint32_t* c1,
+                                                       const uint32_t* c2, int kk) {
+    const code_pos p = locate_code(3, kk);
+    if (p.chunk2 == 0) {
+        const uint32_t* c = p.chunk == 0 ? c0 : (p.chunk == 1 ? c1 : c2);
+        return (c[p.word] >> p.shift) & 7u;
+    }
+    return ((c0[p.word] >> p.shift) & 1u) | (((c1[p.word] >> p.shift) & 1u) << 1) |
+           (((c2[p.word] >> p.shift) & 1u) << 2);
 }
 
 // ---------------------------------------------------------------------------
@@ -134,9 +167,8 @@ __device__ __forceinline__ void load_slice(uint32_t row_chunks, int slice,
         const uint4 q = lds128(row_chunks + slice * 2048);
         o.w[0] = q.x; o.w[1] = q.y; o.w[2] = q.z; o.w[3] = q.w;
     } else if constexpr (BITS == 3) {
-        const uint2 lo = lds64(row_chunks + (slice >> 1) * 2048 + 8 * (slice & 1));
-        o.w[0] = lo.x; o.w[1] = lo.y;
-        o.w[2] = lds32(row_chunks + 2 * 2048 + 4 * slice);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) o.w[c] = lds32(row_chunks + c * 2048 + 4 * slice);
     } else if constexpr (BITS == 8) {
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
@@ -165,14 +197,15 @@ __device__ __forceinline__ void convert_slice(const slice_words<BITS>& in, float
                     lop3_and_or(in.w[j] >> (4 * p), 0x000F000Fu, kMagic128), negoff2, s2, z2);
     } else if constexpr (BITS == 3) {
         constexpr uint32_t negoff2 = SYM ? 0xC303C303u : 0xC300C300u;
-        const uint32_t hb = in.w[2];
 #pragma unroll
-        for (int p = 0; p < 16; ++p) {
-            const uint32_t lw = p < 8 ? in.w[0] : in.w[1];
-            const uint32_t a = lop3_and_or(lw >> (2 * (p & 7)), 0x00030003u, kMagic128);
-            const uint32_t h = (p >= 2) ? (hb >> (p - 2)) : (hb << (2 - p));
-            out[p] = finish_pair<SYM>(lop3_and_or(h, 0x00040004u, a), negoff2, s2, z2);
-        }
+        for (int w = 0; w < 3; ++w)
+#pragma unroll
+            for (int p = 0; p < 5; ++p)
+                out[5 * w + p] = finish_pair<SYM>(
+                    lop3_and_or(in.w[w] >> (3 * p), 0x00070007u, kMagic128), negoff2, s2, z2);
+        const uint32_t b01 = lop3_and_or(in.w[1] >> 14, 0x00020002u,
+                                         lop3_and_or(in.w[0] >> 15, 0x00010001u, kMagic128));
+        out[15] = finish_pair<SYM>(lop3_and_or(in.w[2] >> 13, 0x00040004u, b01), negoff2, s2, z2);
     } else if constexpr (BITS == 8) {
         const float off = SYM ? 8388608.0f + 127.0f : 8388608.0f;
 #pragma unroll
@@ -211,22 +244,11 @@ __device__ __forceinline__ void dequant_slice32(const uint8_t* row_chunks,
                 out[4 * j + p] = finish_pair<SYM>(v, negoff2, s2, z2);
             }
     } else if constexpr (BITS == 3) {
-        constexpr uint32_t negoff2 =
-            SYM ? 0xC303C303u /* -131 */ : 0xC300C300u /* -128 */;
-        // slice 0..3 covers kk [32*slice, +32): low planes chunk slice/2,
-        // words 2*(slice&1), +1; high plane chunk 2, word slice.
-        const uint4 lo = *reinterpret_cast<const uint4*>(row_chunks + (slice >> 1) * 2048);
-        const uint32_t hb = *reinterpret_cast<const uint32_t*>(row_chunks + 2 * 2048 + 4 * slice);
-        const uint32_t l0 = (slice & 1) ? lo.z : lo.x;
-        const uint32_t l1 = (slice & 1) ? lo.w : lo.y;
+        slice_words<3> in;
 #pragma unroll
-        for (int p = 0; p < 16; ++p) {
-            const uint32_t lw = p < 8 ? l0 : l1;
-            const uint32_t a = lop3_and_or(lw >> (2 * (p & 7)), 0x00030003u, kMagic128);
-            const uint32_t h = (p >= 2) ? (hb >> (p - 2)) : (hb << (2 - p));
-            const uint32_t v = lop3_and_or(h, 0x00040004u, a);
-            out[p] = finish_pair<SYM>(v, negoff2, s2, z2);
-        }
+        for (int c = 0; c < 3; ++c)
+            in.w[c] = *reinterpret_cast<const uint32_t*>(row_chunks + c * 2048 + 4 * slice);
+        convert_slice<3, SYM>(in, s, z, s2, z2, out);
     } else if constexpr (BITS == 8) {
         // fp32 magic 2^23: float bits 0x4B0000xx == 8388608 + xx exactly.
         const float off = SYM ? 8388608.0f + 127.0f : 8388608.0f;
