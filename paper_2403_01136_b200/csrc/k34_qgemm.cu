@@ -573,15 +573,22 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
 
             if constexpr (kSK) if (sg.nseg > 1) {
                 const int tr5 = warp == C::kEpiWarp0 && lane == 0 ? 5 : 99;
-                __threadfence();
+                // ticket: bar.sync orders all 128 threads' partial stores
+                // before one thread's acq_rel RMW (release for ours, acquire
+                // of the other segments' for the last arriver) -- the
+                // CUTLASS split-K semaphore pattern; one gpu-scope
+                // synchronisation instead of a fence.sc in every thread
                 trace_ev(a, tr5, ut, 0);
                 asm volatile("bar.sync 1, 128;" ::: "memory");
-                if (warp == C::kEpiWarp0 && lane == 0)
-                    *bcast = atomicAdd(&a.counters[sg.tile], 1u);
+                if (warp == C::kEpiWarp0 && lane == 0) {
+                    unsigned old;
+                    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                                 : "=r"(old) : "l"(&a.counters[sg.tile]) : "memory");
+                    *bcast = old;
+                }
                 asm volatile("bar.sync 1, 128;" ::: "memory");
                 trace_ev(a, tr5, ut, 1);
                 if (*bcast == static_cast<unsigned>(sg.nseg - 1)) {
-                    __threadfence();
                     trace_ev(a, tr5, ut, 2);
                     // ordered reduction of all segments of this tile (row r), 16
                     // tokens at a time. The partial loads of kRB segments are
