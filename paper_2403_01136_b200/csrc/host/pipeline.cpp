@@ -180,6 +180,12 @@ struct pipeline::impl {
     void* scr_f = nullptr;       // [M x h2]
     std::vector<void*> dec_x;    // per group [xi_g x h1]
     std::vector<void*> fb;       // last rank (world > 1): gather target per group
+    // K3 fused (default): one hp_decode_plan per decode group, bound to
+    // dec_x[g]; a decode unit = one persistent launch per bit-width run of
+    // the stage's layers (k3_stage.cu) instead of 6 launches per layer
+    std::vector<hp_decode_plan*> dplans;
+    int dplan_runs = 0;              // kernel launches per fused decode unit
+    cudaEvent_t dec_ev[2] = {nullptr, nullptr};  // instrumented fused unit
     void* ws = nullptr;
     size_t ws_bytes = 0;
     int64_t weight_bytes = 0;
@@ -319,6 +325,23 @@ struct pipeline::impl {
             cuda_ok(cudaMemsetAsync(ws, 0, ws_bytes, cs), "ws");
         }
 
+        if (!opt.decode_per_op) {
+            std::vector<hp_decoder_layer> dl(layers.size());
+            for (size_t li = 0; li < layers.size(); ++li) {
+                for (int o = 0; o < 4; ++o) dl[li].ops[o] = layers[li].ops[o].w;
+                for (int j = 0; j < 4; ++j) dl[li].ln[j] = layers[li].ln[j];
+                if (li == 0 || layers[li].bits != layers[li - 1].bits) ++dplan_runs;
+            }
+            for (int g = 0; g < sched.num_groups; ++g) {
+                hp_decode_plan* dp = nullptr;
+                hp_ok(hp_decode_plan_create(dl.data(), static_cast<int>(dl.size()), dec_x[g],
+                                            group_size[g], &dp),
+                      "decode_plan_create");
+                dplans.push_back(dp);
+            }
+            for (cudaEvent_t* e : {&dec_ev[0], &dec_ev[1]}) cuda_ok(cudaEventCreate(e), "ev");
+        }
+
         load_kernels();
         if (world > 1) connect_links();
 
@@ -378,8 +401,15 @@ struct pipeline::impl {
         if (evs) cuda_ok(timing_record(evs[1], cs), "ev");
     }
 
-    // forward of this stage's layers, in place on x [m x h1]
-    void forward(void* x, int64_t m, int phase, bool instrument) {
+    // forward of this stage's layers, in place on x [m x h1]; a decode unit
+    // of group g >= 0 runs the group's K3-fused plan (bound to dec_x[g])
+    void forward(void* x, int64_t m, int phase, bool instrument, int group = -1) {
+        if (phase == HP_DECODE && group >= 0 && !dplans.empty()) {
+            if (instrument) cuda_ok(timing_record(dec_ev[0], cs), "ev");
+            hp_ok(hp_decode_plan_run(dplans[group], cs), "decode_plan_run");
+            if (instrument) cuda_ok(timing_record(dec_ev[1], cs), "ev");
+            return;
+        }
         for (size_t li = 0; li < layers.size(); ++li) {
             const layer& L = layers[li];
             cudaEvent_t* ev = instrument ? &op_ev[phase][li * 8] : nullptr;
@@ -418,6 +448,11 @@ struct pipeline::impl {
         cuda_ok(cudaMalloc(&x, static_cast<size_t>(rows) * h1 * 2 * 2), "cudaMalloc scratch");
         cuda_ok(hp::launch_synth(x, rows * h1, seed_for({5}), 0.0, 1.0, cs), "synth scratch");
         for (const auto& sh : shapes) forward(x, sh.first, sh.second, false);
+        for (int g = 0; g < static_cast<int>(dplans.size()); ++g) {
+            forward(dec_x[g], group_size[g], HP_DECODE, false, g);
+            cuda_ok(cudaMemsetAsync(dec_x[g], 0, static_cast<size_t>(group_size[g]) * h1 * 2, cs),
+                    "memset");
+        }
         cuda_ok(hp::launch_gather_rows(x, h1, 1, 0, 1, static_cast<int>(h1),
                                        static_cast<char*>(x) + static_cast<size_t>(rows) * h1 * 2, h1,
                                        cs),
@@ -527,7 +562,8 @@ struct pipeline::impl {
             const int64_t m = pre ? prefill_rows(u.index) : group_size[u.index];
             const int phase = pre ? HP_PREFILL : HP_DECODE;
             cuda_ok(timing_record(unit_ev[2 * ui], cs), "ev");
-            forward(x, m, phase, opt.instrument && instr_unit[phase] == static_cast<int>(ui));
+            forward(x, m, phase, opt.instrument && instr_unit[phase] == static_cast<int>(ui),
+                    pre ? -1 : u.index);
             cuda_ok(timing_record(unit_ev[2 * ui + 1], cs), "ev");
 
             // ---- output
@@ -697,6 +733,23 @@ struct pipeline::impl {
             if (ui < 0) continue;
             const unit_ref& u = units[ui];
             const int64_t m = ph == 0 ? prefill_rows(u.index) : group_size[u.index];
+            if (ph == 1 && !dplans.empty()) {
+                // K3 fused: one timed span over the unit's launches; per-layer
+                // decode costs need decode_per_op (tools/layer_costs.py)
+                float ms = 0.f;
+                cuda_ok(cudaEventElapsedTime(&ms, dec_ev[0], dec_ev[1]), "elapsed fused");
+                double info[4];
+                hp_ok(hp_decode_plan_info(dplans[u.index], info), "decode_plan_info");
+                kernel_stats& k = kstats[1];
+                k.launches += dplan_runs;
+                k.seconds += ms * 1e-3;
+                k.bytes += info[1];
+                for (size_t li = 0; li < layers.size(); ++li) {
+                    layer_s[1][li] = 0.0;
+                    for (int o = 0; o < 4; ++o) k.flops += 2.0 * m * shp[o].n * shp[o].k;
+                }
+                continue;
+            }
             for (size_t li = 0; li < layers.size(); ++li) {
                 float ms = 0.f;
                 cuda_ok(cudaEventElapsedTime(&ms, lay_ev[ph][2 * li], lay_ev[ph][2 * li + 1]),
@@ -756,6 +809,9 @@ struct pipeline::impl {
         for (void* p : dec_x) f(p);
         for (void* p : fb) f(p);
         f(ws);
+        for (hp_decode_plan* dp : dplans) hp_decode_plan_destroy(dp);
+        for (cudaEvent_t e : dec_ev)
+            if (e) cudaEventDestroy(e);
         for (auto* v : {&unit_ev, &recv_ev, &comp_ev, &op_ev[0], &op_ev[1], &lay_ev[0], &lay_ev[1]})
             for (cudaEvent_t e : *v) cudaEventDestroy(e);
         for (cudaEvent_t e : {ev_t0, ev_t1, ev_fork, ev_join_s, ev_join_r})
@@ -825,10 +881,10 @@ std::int64_t pipeline::weight_bytes() const { return p_->weight_bytes; }
 
 int pipeline::num_kernel_launches_per_round() const {
     int n = 0;
-    for (const unit_ref& u : p_->units) {
-        n += static_cast<int>(p_->layers.size()) * 6;
-        (void)u;
-    }
+    for (const unit_ref& u : p_->units)
+        n += (u.kind == pipesim::unit_kind::decode && !p_->dplans.empty())
+                 ? p_->dplan_runs
+                 : static_cast<int>(p_->layers.size()) * 6;
     if (p_->rank == p_->world - 1)
         for (const unit_ref& u : p_->units)
             if (u.kind == pipesim::unit_kind::prefill) ++n;  // gather (>=1)

@@ -127,3 +127,23 @@ def test_host_prompt_path(cuda):
     pipe.run(host_in.data_ptr(), b.data_ptr())
     assert torch.equal(a, b)  # same bits whether the prompt was resident or uploaded
     pipe.close()
+
+
+def test_fused_decode_bit_identical_to_per_op(cuda):
+    """K3 fused decode units (default: one persistent launch per bit-width run
+    of the stage) produce the same bits as per-op K3 launches; the mixed 4/8
+    plan makes the stage several runs."""
+    import torch
+    from paper_2403_01136_b200.pipeline import Pipeline
+    plan, model_json = _plan(5)
+    outs, launches = [], []
+    for per_op in (False, True):
+        pipe = Pipeline(json.dumps(plan), model_json, decode_per_op=per_op, instrument=True)
+        o = torch.empty(8 * H1, dtype=torch.bfloat16).pin_memory()
+        pipe.run(None, o.data_ptr())
+        pipe.run(None, o.data_ptr())
+        outs.append(o.clone())
+        launches.append(pipe.info()["launches_per_round"])
+        pipe.close()
+    assert torch.equal(outs[0], outs[1])
+    assert launches[0] < launches[1]
