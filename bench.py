@@ -191,6 +191,8 @@ def main():
     ap.add_argument("--plan", default=None, help="override plan fixture name")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graphs", action="store_true")
+    ap.add_argument("--decode-fused", action="store_true",
+                    help="decode units as one K3-fused launch per bit-width run (hp_decode_plan)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", 0))
@@ -222,7 +224,8 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         ids = obj[0]
     pipe = Pipeline(plan_json, model_json, rank, world, ids, use_graphs=not args.no_graphs,
-                    instrument=True, sm_budget=140 if world > 1 else 0)
+                    instrument=True, sm_budget=140 if world > 1 else 0,
+                    decode_fused=args.decode_fused)
     info = pipe.info()
     h1 = {"opt-13b": 5120, "opt-30b": 7168, "opt-66b": 9216, "bloom-176b": 14336}.get(
         json.loads(model_json).get("preset", ""), json.loads(model_json).get("h1", 0))
@@ -317,7 +320,9 @@ def main():
                                    "avg_flops": d_pre["flops"] / max(d_pre["launches"], 1),
                                    "avg_s": d_pre["seconds"] / max(d_pre["launches"], 1)},
                     "share_of_step": pre_share}
-        roof_dec = {"kernel": "K3 decode dequant-GEMV (hp::qgemm_kernel, BN=32, split-K)",
+        roof_dec = {"kernel": ("K3 fused decode step (hp::dstage_kernel, one launch per bit-width run)"
+                               if args.decode_fused else
+                               "K3 decode dequant-GEMV (hp::qgemm_kernel, BN=32, split-K)"),
                     "bound": "hbm", "achieved": k3, "peak": hbm, "unit": "GB/s",
                     "frac": k3 / hbm if k3 else None, "frac_of_nominal_8TBs": k3 / 8000 if k3 else None,
                     "traffic": traffic("k3"), "traffic_capture": traffic_note("k3"),
@@ -362,7 +367,7 @@ def main():
                        "stages": [st["layers"] for st in plan["stages"]],
                        "l2": "inputs larger than L2 (packed weights "
                              f"{info['weight_bytes'] / 1e9:.1f} GB/rank >> 126 MB)",
-                       "graphs": not args.no_graphs},
+                       "graphs": not args.no_graphs, "decode_fused": args.decode_fused},
             "decode_tok_s": B * (n - 1) / dec_busy if dec_busy > 0 else None,
             "prefill_tok_s": B * s / pre_busy if pre_busy > 0 else None,
             "generated_tok_s": B * n / step_s,

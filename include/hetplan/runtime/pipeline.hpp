@@ -43,8 +43,8 @@ struct pipeline_options {
     double timeout_s = 0.0;     // run() watchdog (0 = wait forever); on
                                 // expiry throws pipeline_timeout with the
                                 // per-stream progress of the stuck round
-    bool decode_per_op = false; // decode units as per-op launches instead of
-                                // one K3-fused launch per bit-width run
+    bool decode_fused = false;  // decode units as one K3-fused launch per
+                                // bit-width run instead of per-op launches
 };
 
 // run() exceeded pipeline_options::timeout_s (hp_pipeline_run -> HP_ETIMEOUT).

@@ -186,10 +186,12 @@ typedef struct {
     double timeout_s;    /* hp_pipeline_run watchdog, 0 = none; expiry ->
                           * HP_ETIMEOUT with per-stream progress in
                           * hp_last_error (destroy the pipeline after)     */
-    int32_t decode_per_op;  /* 0 (default): each decode unit of the stage is
-                          * ONE K3-fused launch per bit-width run
-                          * (hp_decode_plan); 1: per-op hp_layernorm +
-                          * hp_qlinear launches (per-layer decode costs)  */
+    int32_t decode_fused; /* 0 (default): a decode unit is per-op launches
+                          * (hp_layernorm + 4 hp_qlinear per layer, PDL
+                          * chained); 1: ONE K3-fused persistent launch per
+                          * bit-width run of the stage (hp_decode_plan;
+                          * bit-identical, slower on B200 today, see
+                          * DESIGN.md §4.3)                               */
 } hp_pipeline_options;
 hp_status hp_nccl_unique_id(void* out128);
 hp_status hp_pipeline_create(const char* plan_json, const char* model_json, int rank,

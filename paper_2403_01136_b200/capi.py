@@ -61,7 +61,7 @@ class hp_pipeline_options(C.Structure):
         ("seed", C.c_uint64),
         ("weight_std", C.c_double),
         ("timeout_s", C.c_double),
-        ("decode_per_op", C.c_int32),
+        ("decode_fused", C.c_int32),
     ]
 
 

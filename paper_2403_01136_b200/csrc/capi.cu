@@ -267,7 +267,17 @@ hp_status hp_indicator_stats(const void* w, int64_t n_out, int64_t k_in, int64_t
         return fail(HP_EINVAL, "indicator_stats: bad calibration shape");
     if (hp_status s = need_device()) return s;
     auto st = static_cast<cudaStream_t>(stream);
-    const int nbw = 296, nbx = x ? 296 : 0;
+    // ~8 blocks of 256 threads per SM, split between W and X by bytes
+    int sms = 148;
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const double wb = static_cast<double>(n_out) * k_in, xb = x ? static_cast<double>(tokens) * k_in : 0.0;
+    const int nb = 8 * sms;
+    const int nbx = x ? std::max(1, std::min(nb - 1, static_cast<int>(nb * xb / (wb + xb)))) : 0;
+    const int nbw = std::max(1, nb - nbx);
     const size_t bytes = hp::stats_scratch_bytes(nbw, nbx);
     void* scratch = nullptr;
     cudaError_t e = cudaMallocAsync(&scratch, bytes, st);

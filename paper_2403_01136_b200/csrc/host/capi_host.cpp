@@ -284,7 +284,7 @@ hp_status hp_pipeline_create(const char* plan_json, const char* model_json, int 
             po.seed = opt->seed;
             po.weight_std = opt->weight_std > 0 ? opt->weight_std : 0.02;
             po.timeout_s = opt->timeout_s;
-            po.decode_per_op = opt->decode_per_op != 0;
+            po.decode_fused = opt->decode_fused != 0;
         }
         std::vector<std::array<char, 128>> ids;
         if (world > 1) {

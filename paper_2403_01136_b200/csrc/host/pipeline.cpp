@@ -180,7 +180,7 @@ struct pipeline::impl {
     void* scr_f = nullptr;       // [M x h2]
     std::vector<void*> dec_x;    // per group [xi_g x h1]
     std::vector<void*> fb;       // last rank (world > 1): gather target per group
-    // K3 fused (default): one hp_decode_plan per decode group, bound to
+    // K3 fused (option decode_fused): one hp_decode_plan per decode group, bound to
     // dec_x[g]; a decode unit = one persistent launch per bit-width run of
     // the stage's layers (k3_stage.cu) instead of 6 launches per layer
     std::vector<hp_decode_plan*> dplans;
@@ -325,7 +325,7 @@ struct pipeline::impl {
             cuda_ok(cudaMemsetAsync(ws, 0, ws_bytes, cs), "ws");
         }
 
-        if (!opt.decode_per_op) {
+        if (opt.decode_fused) {
             std::vector<hp_decoder_layer> dl(layers.size());
             for (size_t li = 0; li < layers.size(); ++li) {
                 for (int o = 0; o < 4; ++o) dl[li].ops[o] = layers[li].ops[o].w;
@@ -735,7 +735,7 @@ struct pipeline::impl {
             const int64_t m = ph == 0 ? prefill_rows(u.index) : group_size[u.index];
             if (ph == 1 && !dplans.empty()) {
                 // K3 fused: one timed span over the unit's launches; per-layer
-                // decode costs need decode_per_op (tools/layer_costs.py)
+                // decode costs need per-op decode (tools/layer_costs.py)
                 float ms = 0.f;
                 cuda_ok(cudaEventElapsedTime(&ms, dec_ev[0], dec_ev[1]), "elapsed fused");
                 double info[4];

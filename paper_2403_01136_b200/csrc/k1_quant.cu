@@ -75,94 +75,113 @@ __device__ __forceinline__ int quant_code(float w, const group_grid& g) {
     return static_cast<int>(sn);
 }
 
-// One CTA = one 128x128 tile; thread r owns row r.
+// One thread per (row, 32-k slice): a warp covers 8 rows x one 128-k group
+// (lane = 4 * row + slice), a 256-thread CTA 64 rows of one group. Each
+// thread loads its slice with 4 independent 16-byte loads, the group's
+// min/max is a 2-step shuffle over the 4 lanes of the row, and the thread
+// emits exactly its slice's part of the tile layout (layout.cuh): 4-bit one
+// 16 B row entry of chunk s, 8-bit two (chunks 2s, 2s+1), 3-bit word s of
+// chunks 0..2, 16-bit four. For a fixed chunk the 8 rows of a warp are 128
+// contiguous bytes, so every store instruction writes whole lines.
+constexpr int kQRows = 64;  // rows per CTA
+
 template <int BITS>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(256)
     quant_pack_kernel(const __nv_bfloat16* __restrict__ w, int64_t n_out,
                       int64_t k_in, int64_t ldw, int G, int sym,
                       uint8_t* __restrict__ packed, float* __restrict__ scale,
                       float* __restrict__ zero, double* __restrict__ step64,
                       double* __restrict__ zero64) {
-    constexpr int kPad = 8;  // bf16 elements of row padding (bank spread)
-    __shared__ __align__(16) __nv_bfloat16 tile[128][128 + kPad];
+    const int lane = threadIdx.x & 31;
+    const int sl = lane & 3;
     const int g = blockIdx.x;
-    const int64_t nt = blockIdx.y;
-    const int r = threadIdx.x;
-    const int64_t row0 = nt * 128;
-    const int64_t k0 = static_cast<int64_t>(g) * 128;
-    const int cnt = static_cast<int>(k_in - k0 < 128 ? k_in - k0 : 128);
-    const bool vec_ok = (cnt == 128) && (ldw % 8 == 0) &&
-                        ((reinterpret_cast<uintptr_t>(w) & 15) == 0);
+    const int64_t row = static_cast<int64_t>(blockIdx.y) * kQRows + (threadIdx.x >> 5) * 8 + (lane >> 2);
+    const int64_t nt = row >> 7;
+    const int r = static_cast<int>(row & 127);
+    const int64_t k0 = static_cast<int64_t>(g) * 128 + sl * 32;
+    const int cnt = static_cast<int>(k_in - k0 <= 0 ? 0 : (k_in - k0 < 32 ? k_in - k0 : 32));
+    const bool row_ok = row < n_out;
+    const int valid = row_ok ? cnt : 0;
 
-    // coalesced load: 16 lanes cover one row's 256 bytes
-    if (vec_ok) {
-#pragma unroll 4
-        for (int q = r; q < 128 * 16; q += 128) {
-            const int rr = q >> 4, cc = q & 15;
-            uint4 v = make_uint4(0, 0, 0, 0);
-            if (row0 + rr < n_out)
-                v = __ldg(reinterpret_cast<const uint4*>(w + (row0 + rr) * ldw + k0) + cc);
-            *reinterpret_cast<uint4*>(&tile[rr][cc * 8]) = v;
+    // slice values (padding = 0, excluded from min/max)
+    uint32_t v[16];
+    const __nv_bfloat16* src = w + row * ldw + k0;
+    if (valid == 32 && (ldw % 8 == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+        uint4 q[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) q[i] = __ldcs(reinterpret_cast<const uint4*>(src) + i);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            v[4 * i] = q[i].x; v[4 * i + 1] = q[i].y; v[4 * i + 2] = q[i].z; v[4 * i + 3] = q[i].w;
         }
     } else {
-        for (int q = r; q < 128 * 128; q += 128) {
-            const int rr = q >> 7, cc = q & 127;
-            __nv_bfloat16 v = __float2bfloat16(0.0f);
-            if (row0 + rr < n_out && cc < cnt) v = w[(row0 + rr) * ldw + k0 + cc];
-            tile[rr][cc] = v;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const uint32_t lo = 2 * i < valid ? __bfloat16_as_ushort(src[2 * i]) : 0u;
+            const uint32_t hi = 2 * i + 1 < valid ? __bfloat16_as_ushort(src[2 * i + 1]) : 0u;
+            v[i] = lo | (hi << 16);
         }
     }
-    __syncthreads();
-
-    const bool row_ok = row0 + r < n_out;
-    const size_t sidx = (static_cast<size_t>(nt) * G + g) * 128 + r;
+    auto elem = [&](int e) { return __uint_as_float((e & 1) ? (v[e >> 1] & 0xFFFF0000u) : (v[e >> 1] << 16)); };
     uint8_t* tbase = packed + (static_cast<size_t>(nt) * G + g) * tile_bytes(BITS) + r * 16;
 
     if constexpr (BITS == 16) {
+        // padding rows of the last tile (row >= n_out) are written as zeros
 #pragma unroll
-        for (int c = 0; c < 16; ++c)
-            *reinterpret_cast<uint4*>(tbase + c * 2048) =
-                *reinterpret_cast<const uint4*>(&tile[r][c * 8]);
-        return;
+        for (int c = 0; c < 4; ++c)
+            *reinterpret_cast<uint4*>(tbase + (4 * sl + c) * 2048) =
+                make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
     } else {
-        float wmin = 0.0f, wmax = 0.0f;
-        if (row_ok) {
-            wmin = __bfloat162float(tile[r][0]);
-            wmax = wmin;
-            for (int k = 1; k < cnt; ++k) {
-                const float v = __bfloat162float(tile[r][k]);
-                wmin = fminf(wmin, v);
-                wmax = fmaxf(wmax, v);
+        float wmin = __int_as_float(0x7f800000), wmax = -__int_as_float(0x7f800000);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+            if (e < valid) {
+                wmin = fminf(wmin, elem(e));
+                wmax = fmaxf(wmax, elem(e));
             }
         }
+        wmin = fminf(wmin, __shfl_xor_sync(0xffffffffu, wmin, 1));
+        wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, 1));
+        wmin = fminf(wmin, __shfl_xor_sync(0xffffffffu, wmin, 2));
+        wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, 2));
+        if (!row_ok) wmin = wmax = 0.0f;
         const group_grid gg = make_grid(wmin, wmax, BITS, sym != 0);
         const int off = sym ? (1 << (BITS - 1)) - 1 : 0;
-        if (scale) scale[sidx] = row_ok ? static_cast<float>(gg.step) : 0.0f;
-        if (zero) zero[sidx] = row_ok ? gg.zero_f : 0.0f;
-        if (row_ok && step64) {
-            step64[(row0 + r) * G + g] = gg.step;
-            zero64[(row0 + r) * G + g] = gg.zero;
+        if (sl == 0) {
+            const size_t sidx = (static_cast<size_t>(nt) * G + g) * 128 + r;
+            if (scale) scale[sidx] = row_ok ? static_cast<float>(gg.step) : 0.0f;
+            if (zero) zero[sidx] = row_ok ? gg.zero_f : 0.0f;
+            if (row_ok && step64) {
+                step64[row * G + g] = gg.step;
+                zero64[row * G + g] = gg.zero;
+            }
         }
-
-        uint32_t words[BITS * 4];
+        // slice-local words: codes e < 32 of this slice at the positions
+        // locate_code gives for kk = e (the slice index only selects where
+        // the words land, below)
+        uint32_t words[BITS == 3 ? 12 : BITS];
 #pragma unroll
-        for (int i = 0; i < BITS * 4; ++i) words[i] = 0;
-#pragma unroll 8
-        for (int kk = 0; kk < 128; ++kk) {
-            int q = 0;  // padding / invalid rows: signed code 0
-            if (row_ok && kk < cnt) q = quant_code(__bfloat162float(tile[r][kk]), gg);
+        for (int i = 0; i < (BITS == 3 ? 12 : BITS); ++i) words[i] = 0;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+            const int q = e < valid ? quant_code(elem(e), gg) : 0;  // padding: signed code 0
             const uint32_t sc = static_cast<uint32_t>(q + off);
             if constexpr (BITS == 3) {
-                put_code3(words, kk, sc);
+                put_code3(words, e, sc);
             } else {
-                const code_pos p = locate_code(BITS, kk);
+                const code_pos p = locate_code(BITS, e);
                 words[p.chunk * 4 + p.word] |= sc << p.shift;
             }
         }
+        if constexpr (BITS == 4) {
+            *reinterpret_cast<uint4*>(tbase + sl * 2048) = make_uint4(words[0], words[1], words[2], words[3]);
+        } else if constexpr (BITS == 8) {
+            *reinterpret_cast<uint4*>(tbase + (2 * sl) * 2048) = make_uint4(words[0], words[1], words[2], words[3]);
+            *reinterpret_cast<uint4*>(tbase + (2 * sl + 1) * 2048) = make_uint4(words[4], words[5], words[6], words[7]);
+        } else {
 #pragma unroll
-        for (int c = 0; c < BITS; ++c)
-            *reinterpret_cast<uint4*>(tbase + c * 2048) =
-                make_uint4(words[4 * c], words[4 * c + 1], words[4 * c + 2], words[4 * c + 3]);
+            for (int b = 0; b < 3; ++b) *reinterpret_cast<uint32_t*>(tbase + b * 2048 + sl * 4) = words[b * 4];
+        }
     }
 }
 
@@ -250,14 +269,15 @@ cudaError_t launch_quant_pack(const void* w, int64_t n_out, int64_t k_in,
                               float* scale, float* zero, double* step64,
                               double* zero64, cudaStream_t st) {
     const int G = static_cast<int>(ceil_div64(k_in, 128));
-    const dim3 grid(G, static_cast<unsigned>(ceil_div64(n_out, 128)));
+    // rows up to the 128-row tile boundary: padding rows get code 0 / scale 0
+    const dim3 grid(G, static_cast<unsigned>(ceil_div64(n_out, 128) * (128 / kQRows)));
     auto* wp = static_cast<const __nv_bfloat16*>(w);
     auto* pp = static_cast<uint8_t*>(packed);
     switch (bits) {
-        case 3: quant_pack_kernel<3><<<grid, 128, 0, st>>>(wp, n_out, k_in, ldw, G, sym, pp, scale, zero, step64, zero64); break;
-        case 4: quant_pack_kernel<4><<<grid, 128, 0, st>>>(wp, n_out, k_in, ldw, G, sym, pp, scale, zero, step64, zero64); break;
-        case 8: quant_pack_kernel<8><<<grid, 128, 0, st>>>(wp, n_out, k_in, ldw, G, sym, pp, scale, zero, step64, zero64); break;
-        case 16: quant_pack_kernel<16><<<grid, 128, 0, st>>>(wp, n_out, k_in, ldw, G, sym, pp, scale, zero, step64, zero64); break;
+        case 3: quant_pack_kernel<3><<<grid, 256, 0, st>>>(wp, n_out, k_in, ldw, G, sym, pp, scale, zero, step64, zero64); break;
+        case 4: quant_pack_kernel<4><<<grid, 256, 0, st>>>(wp, n_out, k_in, ldw, G, sym, pp, scale, zero, step64, zero64); break;
+        case 8: quant_pack_kernel<8><<<grid, 256, 0, st>>>(wp, n_out, k_in, ldw, G, sym, pp, scale, zero, step64, zero64); break;
+        case 16: quant_pack_kernel<16><<<grid, 256, 0, st>>>(wp, n_out, k_in, ldw, G, sym, pp, scale, zero, step64, zero64); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

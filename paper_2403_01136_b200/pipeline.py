@@ -45,9 +45,9 @@ class Pipeline:
                  ids: bytes | None = None, scheme: int = capi.HP_SYMMETRIC,
                  use_graphs: bool = True, instrument: bool = False, sm_budget: int = 0,
                  seed: int = 2403, weight_std: float = 0.02, timeout_s: float = 0.0,
-                 decode_per_op: bool = False):
+                 decode_fused: bool = False):
         opt = capi.hp_pipeline_options(scheme, int(use_graphs), int(instrument), sm_budget,
-                                       seed, weight_std, timeout_s, int(decode_per_op))
+                                       seed, weight_std, timeout_s, int(decode_fused))
         h = C.c_void_p()
         idbuf = C.create_string_buffer(ids, len(ids)) if ids else None
         check(lib.hp_pipeline_create(plan_json.encode(), model_json.encode(), rank, world,

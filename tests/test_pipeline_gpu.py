@@ -130,15 +130,15 @@ def test_host_prompt_path(cuda):
 
 
 def test_fused_decode_bit_identical_to_per_op(cuda):
-    """K3 fused decode units (default: one persistent launch per bit-width run
-    of the stage) produce the same bits as per-op K3 launches; the mixed 4/8
-    plan makes the stage several runs."""
+    """K3 fused decode units (decode_fused: one persistent launch per
+    bit-width run of the stage) produce the same bits as the default per-op
+    K3 launches; the mixed 4/8 plan makes the stage several runs."""
     import torch
     from paper_2403_01136_b200.pipeline import Pipeline
     plan, model_json = _plan(5)
     outs, launches = [], []
-    for per_op in (False, True):
-        pipe = Pipeline(json.dumps(plan), model_json, decode_per_op=per_op, instrument=True)
+    for fused in (True, False):
+        pipe = Pipeline(json.dumps(plan), model_json, decode_fused=fused, instrument=True)
         o = torch.empty(8 * H1, dtype=torch.bfloat16).pin_memory()
         pipe.run(None, o.data_ptr())
         pipe.run(None, o.data_ptr())

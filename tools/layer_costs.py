@@ -26,7 +26,7 @@ def main():
     from paper_2403_01136_b200.pipeline import Pipeline, load_plan
     plan_json, model_json = load_plan(name)
     plan = json.loads(plan_json)
-    p = Pipeline(plan_json, model_json, instrument=True, decode_per_op=True)
+    p = Pipeline(plan_json, model_json, instrument=True)
     for _ in range(3):
         p.run()
     pre, dec = [], []
