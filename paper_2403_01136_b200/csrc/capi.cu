@@ -257,6 +257,29 @@ hp_status hp_dequant(const hp_qweight* w, void* w_bf16, hp_stream stream) {
                        "dequant");
 }
 
+// One memory pool per device for small stream-ordered scratch, with an
+// unbounded release threshold so freed blocks are reused, never unmapped.
+static cudaMemPool_t scratch_pool() {
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    if (!pools[dev]) {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        if (cudaMemPoolCreate(&pools[dev], &props) != cudaSuccess) {
+            cudaGetLastError();
+            cudaDeviceGetDefaultMemPool(&pools[dev], dev);
+        }
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    return pools[dev];
+}
+
 hp_status hp_indicator_stats(const void* w, int64_t n_out, int64_t k_in, int64_t ldw,
                              const void* x, int64_t tokens, int64_t ldx, double* stats5,
                              hp_stream stream) {
@@ -274,13 +297,18 @@ hp_status hp_indicator_stats(const void* w, int64_t n_out, int64_t k_in, int64_t
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    const double wb = static_cast<double>(n_out) * k_in, xb = x ? static_cast<double>(tokens) * k_in : 0.0;
+    // (an X element costs ~4x a W element: fp64 moments vs fp32 min/max, so
+    // X blocks get proportionally fewer bytes and finish with the W blocks)
+    const double wb = static_cast<double>(n_out) * k_in, xb = x ? 4.0 * tokens * k_in : 0.0;
     const int nb = 8 * sms;
     const int nbx = x ? std::max(1, std::min(nb - 1, static_cast<int>(nb * xb / (wb + xb)))) : 0;
     const int nbw = std::max(1, nb - nbx);
     const size_t bytes = hp::stats_scratch_bytes(nbw, nbx);
     void* scratch = nullptr;
-    cudaError_t e = cudaMallocAsync(&scratch, bytes, st);
+    // stream-ordered scratch from a private pool that keeps its memory: a
+    // default-pool cudaMallocAsync/cudaFreeAsync pair re-maps physical pages
+    // at every synchronisation (~2 ms per call, 30x the kernel itself)
+    cudaError_t e = cudaMallocFromPoolAsync(&scratch, bytes, scratch_pool(), st);
     if (e != cudaSuccess) return cuda_status(e, "indicator_stats alloc");
     e = cudaMemsetAsync(scratch, 0, 256, st);
     if (e == cudaSuccess)

@@ -17,6 +17,7 @@
 // weights take the slow path.
 #include <cuda_bf16.h>
 #include <cstdint>
+#include <utility>
 
 #include "layout.cuh"
 
@@ -57,132 +58,240 @@ __device__ __forceinline__ group_grid make_grid(float wmin, float wmax,
     return g;
 }
 
-// Signed grid code of one element (reference quantize() inner loop).
-__device__ __forceinline__ int quant_code(float w, const group_grid& g) {
-    if (g.step == 0.0) return 0;  // flat group: out = zero (indicator.cpp:39-41)
-    const float x = (w - g.zero_f) * g.rcp_f + 0.5f;
-    const float fl = floorf(x);
-    const float fr = x - fl;
-    double sn;
-    if (fr >= kTieMargin && fr <= 1.0f - kTieMargin) {
-        sn = static_cast<double>(fl);
-    } else {
-        const double scaled =
-            __ddiv_rn(__dsub_rn(static_cast<double>(w), g.zero), g.step);
-        sn = floor(__dadd_rn(scaled, 0.5));
-    }
-    sn = sn < g.lo ? g.lo : (g.hi < sn ? g.hi : sn);  // std::clamp
-    return static_cast<int>(sn);
+// Signed grid code of one element on the exact path: the reference's fp64
+// operation sequence (indicator.cpp:44-47) and std::clamp.
+__device__ __noinline__ int quant_code_exact(float w, double step, double zero, double lo, double hi) {
+    if (step == 0.0) return 0;  // flat group: out = zero (indicator.cpp:39-41)
+    const double scaled = __ddiv_rn(__dsub_rn(static_cast<double>(w), zero), step);
+    const double sn = floor(__dadd_rn(scaled, 0.5));
+    return static_cast<int>(sn < lo ? lo : (hi < sn ? hi : sn));
 }
 
-// One thread per (row, 32-k slice): a warp covers 8 rows x one 128-k group
-// (lane = 4 * row + slice), a 256-thread CTA 64 rows of one group. Each
-// thread loads its slice with 4 independent 16-byte loads, the group's
-// min/max is a 2-step shuffle over the 4 lanes of the row, and the thread
-// emits exactly its slice's part of the tile layout (layout.cuh): 4-bit one
-// 16 B row entry of chunk s, 8-bit two (chunks 2s, 2s+1), 3-bit word s of
-// chunks 0..2, 16-bit four. For a fixed chunk the 8 rows of a warp are 128
-// contiguous bytes, so every store instruction writes whole lines.
-constexpr int kQRows = 64;  // rows per CTA
+// The packed words of one 32-k slice are accumulated with one IMAD per code:
+// word += bits(nm) << shift, where nm = xf + 1.5*2^23 holds M + q in its bit
+// pattern (M = 0x4B400000). The words start at the compile-time constant
+// sum over their fields of (off - M) << shift (mod 2^32), so the final word
+// is exactly sum (q + off) << shift, the stored codes of layout.cuh.
+constexpr uint32_t kMagicBits = 0x4B400000u;
+constexpr float kMagicF = 12582912.0f;  // 1.5 * 2^23
 
 template <int BITS>
-__global__ void __launch_bounds__(256)
+struct slice_pack {
+    static constexpr int NW = BITS == 3 ? 12 : BITS;  // words[chunk * 4 + word]
+    // field positions for code e (0..31) of the slice; 3-bit pair 15 sets
+    // three 1-bit fields (bit b of the code in chunk b) and is handled apart
+    __host__ __device__ static constexpr int word_of(int e) {
+        return BITS == 3 ? locate_code(3, e).chunk * 4 + locate_code(3, e).word
+                         : locate_code(BITS, e).chunk * 4 + locate_code(BITS, e).word;
+    }
+    __host__ __device__ static constexpr int shift_of(int e) { return locate_code(BITS, e).shift; }
+    __host__ __device__ static constexpr bool split3(int e) { return BITS == 3 && ((e >> 1) & 15) == 15; }
+    __host__ __device__ static constexpr uint32_t init(int wi, int off) {
+        uint32_t c = 0;
+        for (int e = 0; e < 32; ++e)
+            if (!split3(e) && word_of(e) == wi) c += (static_cast<uint32_t>(off) - kMagicBits) << shift_of(e);
+        return c;
+    }
+    template <int OFF, int... I>
+    __device__ static __forceinline__ void init_words(uint32_t* w, std::integer_sequence<int, I...>) {
+        ((w[I] = std::integral_constant<uint32_t, init(I, OFF)>::value), ...);
+    }
+    __device__ static __forceinline__ void init_words(uint32_t* w, bool sym) {
+        if (sym)
+            init_words<(1 << (BITS - 1)) - 1>(w, std::make_integer_sequence<int, NW>{});
+        else
+            init_words<0>(w, std::make_integer_sequence<int, NW>{});
+    }
+};
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Work item = (64-row block, 128-k group); one thread per (row, 32-k slice):
+// a warp covers 8 rows x one group (lane = 4 * row + slice), a 256-thread
+// CTA 64 rows. CTAs walk items grid-stride; each thread streams its own 64
+// slice bytes into shared memory with cp.async kD-1 items ahead, so HBM
+// reads overlap the arithmetic without holding registers. The group's
+// min/max is a 2-step shuffle over the 4 lanes of a row, and each thread
+// emits exactly its slice's part of the tile layout (layout.cuh): 4-bit one
+// 16 B row entry of chunk s, 8-bit two (chunks 2s, 2s+1), 3-bit word s of
+// chunks 0..2, 16-bit four; for a fixed chunk the 8 rows of a warp are 128
+// contiguous bytes, so every store instruction writes whole lines.
+constexpr int kQRows = 64;  // rows per item
+constexpr int kD = 3;       // cp.async pipeline depth (items)
+
+template <int BITS>
+__global__ void __launch_bounds__(256, 3)
     quant_pack_kernel(const __nv_bfloat16* __restrict__ w, int64_t n_out,
-                      int64_t k_in, int64_t ldw, int G, int sym,
+                      int64_t k_in, int64_t ldw, int G, int sym, int64_t items,
                       uint8_t* __restrict__ packed, float* __restrict__ scale,
                       float* __restrict__ zero, double* __restrict__ step64,
                       double* __restrict__ zero64) {
-    const int lane = threadIdx.x & 31;
+    __shared__ __align__(16) uint4 buf[kD][4][256];  // [stage][16 B piece][thread]
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
     const int sl = lane & 3;
-    const int g = blockIdx.x;
-    const int64_t row = static_cast<int64_t>(blockIdx.y) * kQRows + (threadIdx.x >> 5) * 8 + (lane >> 2);
-    const int64_t nt = row >> 7;
-    const int r = static_cast<int>(row & 127);
-    const int64_t k0 = static_cast<int64_t>(g) * 128 + sl * 32;
-    const int cnt = static_cast<int>(k_in - k0 <= 0 ? 0 : (k_in - k0 < 32 ? k_in - k0 : 32));
-    const bool row_ok = row < n_out;
-    const int valid = row_ok ? cnt : 0;
+    const int rin = (tid >> 5) * 8 + (lane >> 2);
+    const bool vec_ok = (ldw % 8 == 0) && ((reinterpret_cast<uintptr_t>(w) & 15) == 0);
+    struct where {
+        int64_t row, k0;
+        int g, valid;
+        bool full;
+    };
+    auto locate = [&](int64_t it) {
+        where q;
+        const int64_t rb = it / G;
+        q.g = static_cast<int>(it - rb * G);
+        q.row = rb * kQRows + rin;
+        q.k0 = static_cast<int64_t>(q.g) * 128 + sl * 32;
+        const int cnt = static_cast<int>(k_in - q.k0 <= 0 ? 0 : (k_in - q.k0 < 32 ? k_in - q.k0 : 32));
+        q.valid = q.row < n_out ? cnt : 0;
+        q.full = vec_ok && q.valid == 32;
+        return q;
+    };
+    auto issue = [&](int64_t it, int stage) {
+        if (it < items) {
+            const where q = locate(it);
+            if (q.full) {
+                const __nv_bfloat16* src = w + q.row * ldw + q.k0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    cp_async16(static_cast<uint32_t>(__cvta_generic_to_shared(&buf[stage][i][tid])),
+                               reinterpret_cast<const uint4*>(src) + i);
+            }
+        }
+        cp_async_commit();  // (possibly empty) group: keeps the wait count uniform
+    };
 
-    // slice values (padding = 0, excluded from min/max)
-    uint32_t v[16];
-    const __nv_bfloat16* src = w + row * ldw + k0;
-    if (valid == 32 && (ldw % 8 == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
-        uint4 q[4];
+    const int64_t step_it = gridDim.x;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) q[i] = __ldcs(reinterpret_cast<const uint4*>(src) + i);
+    for (int d = 0; d < kD - 1; ++d) issue(blockIdx.x + d * step_it, d);
+    int stage = 0;
+    for (int64_t it = blockIdx.x; it < items; it += step_it) {
+        issue(it + (kD - 1) * step_it, (stage + kD - 1) % kD);
+        cp_async_wait<kD - 1>();
+        const where q = locate(it);
+        uint32_t v[16];
+        if (q.full) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            v[4 * i] = q[i].x; v[4 * i + 1] = q[i].y; v[4 * i + 2] = q[i].z; v[4 * i + 3] = q[i].w;
+            for (int i = 0; i < 4; ++i) {
+                const uint4 u = buf[stage][i][tid];
+                v[4 * i] = u.x; v[4 * i + 1] = u.y; v[4 * i + 2] = u.z; v[4 * i + 3] = u.w;
+            }
+        } else {  // ragged k, rows past n_out (tile padding) or unaligned rows
+            const __nv_bfloat16* src = w + q.row * ldw + q.k0;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const uint32_t lo = 2 * i < q.valid ? __bfloat16_as_ushort(src[2 * i]) : 0u;
+                const uint32_t hi = 2 * i + 1 < q.valid ? __bfloat16_as_ushort(src[2 * i + 1]) : 0u;
+                v[i] = lo | (hi << 16);
+            }
         }
-    } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const uint32_t lo = 2 * i < valid ? __bfloat16_as_ushort(src[2 * i]) : 0u;
-            const uint32_t hi = 2 * i + 1 < valid ? __bfloat16_as_ushort(src[2 * i + 1]) : 0u;
-            v[i] = lo | (hi << 16);
-        }
-    }
-    auto elem = [&](int e) { return __uint_as_float((e & 1) ? (v[e >> 1] & 0xFFFF0000u) : (v[e >> 1] << 16)); };
-    uint8_t* tbase = packed + (static_cast<size_t>(nt) * G + g) * tile_bytes(BITS) + r * 16;
+        stage = (stage + 1) % kD;
+        const int64_t nt = q.row >> 7;
+        const int r = static_cast<int>(q.row & 127);
+        uint8_t* tbase = packed + (static_cast<size_t>(nt) * G + q.g) * tile_bytes(BITS) + r * 16;
+        auto elem = [&](int e) { return __uint_as_float((e & 1) ? (v[e >> 1] & 0xFFFF0000u) : (v[e >> 1] << 16)); };
 
-    if constexpr (BITS == 16) {
-        // padding rows of the last tile (row >= n_out) are written as zeros
+        if constexpr (BITS == 16) {
+            // padding rows of the last tile (row >= n_out) are written as zeros
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-            *reinterpret_cast<uint4*>(tbase + (4 * sl + c) * 2048) =
-                make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-    } else {
-        float wmin = __int_as_float(0x7f800000), wmax = -__int_as_float(0x7f800000);
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-            if (e < valid) {
-                wmin = fminf(wmin, elem(e));
-                wmax = fmaxf(wmax, elem(e));
-            }
-        }
-        wmin = fminf(wmin, __shfl_xor_sync(0xffffffffu, wmin, 1));
-        wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, 1));
-        wmin = fminf(wmin, __shfl_xor_sync(0xffffffffu, wmin, 2));
-        wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, 2));
-        if (!row_ok) wmin = wmax = 0.0f;
-        const group_grid gg = make_grid(wmin, wmax, BITS, sym != 0);
-        const int off = sym ? (1 << (BITS - 1)) - 1 : 0;
-        if (sl == 0) {
-            const size_t sidx = (static_cast<size_t>(nt) * G + g) * 128 + r;
-            if (scale) scale[sidx] = row_ok ? static_cast<float>(gg.step) : 0.0f;
-            if (zero) zero[sidx] = row_ok ? gg.zero_f : 0.0f;
-            if (row_ok && step64) {
-                step64[row * G + g] = gg.step;
-                zero64[row * G + g] = gg.zero;
-            }
-        }
-        // slice-local words: codes e < 32 of this slice at the positions
-        // locate_code gives for kk = e (the slice index only selects where
-        // the words land, below)
-        uint32_t words[BITS == 3 ? 12 : BITS];
-#pragma unroll
-        for (int i = 0; i < (BITS == 3 ? 12 : BITS); ++i) words[i] = 0;
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-            const int q = e < valid ? quant_code(elem(e), gg) : 0;  // padding: signed code 0
-            const uint32_t sc = static_cast<uint32_t>(q + off);
-            if constexpr (BITS == 3) {
-                put_code3(words, e, sc);
-            } else {
-                const code_pos p = locate_code(BITS, e);
-                words[p.chunk * 4 + p.word] |= sc << p.shift;
-            }
-        }
-        if constexpr (BITS == 4) {
-            *reinterpret_cast<uint4*>(tbase + sl * 2048) = make_uint4(words[0], words[1], words[2], words[3]);
-        } else if constexpr (BITS == 8) {
-            *reinterpret_cast<uint4*>(tbase + (2 * sl) * 2048) = make_uint4(words[0], words[1], words[2], words[3]);
-            *reinterpret_cast<uint4*>(tbase + (2 * sl + 1) * 2048) = make_uint4(words[4], words[5], words[6], words[7]);
+            for (int c = 0; c < 4; ++c)
+                *reinterpret_cast<uint4*>(tbase + (4 * sl + c) * 2048) =
+                    make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+            continue;
         } else {
+            float wmin, wmax;
+            if (q.full) {  // bf16x2 min/max (exact), halves folded at the end
+                __nv_bfloat162 mn = *reinterpret_cast<const __nv_bfloat162*>(&v[0]), mx = mn;
 #pragma unroll
-            for (int b = 0; b < 3; ++b) *reinterpret_cast<uint32_t*>(tbase + b * 2048 + sl * 4) = words[b * 4];
+                for (int i = 1; i < 16; ++i) {
+                    const __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&v[i]);
+                    mn = __hmin2(mn, h);
+                    mx = __hmax2(mx, h);
+                }
+                wmin = fminf(__low2float(mn), __high2float(mn));
+                wmax = fmaxf(__low2float(mx), __high2float(mx));
+            } else {
+                wmin = __int_as_float(0x7f800000);
+                wmax = -__int_as_float(0x7f800000);
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    if (e < q.valid) {
+                        wmin = fminf(wmin, elem(e));
+                        wmax = fmaxf(wmax, elem(e));
+                    }
+                }
+            }
+            wmin = fminf(wmin, __shfl_xor_sync(0xffffffffu, wmin, 1));
+            wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, 1));
+            wmin = fminf(wmin, __shfl_xor_sync(0xffffffffu, wmin, 2));
+            wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, 2));
+            const bool row_ok = q.row < n_out;
+            if (!row_ok) wmin = wmax = 0.0f;
+            const group_grid gg = make_grid(wmin, wmax, BITS, sym != 0);
+            const int off = sym ? (1 << (BITS - 1)) - 1 : 0;
+            if (sl == 0) {
+                const size_t sidx = (static_cast<size_t>(nt) * G + q.g) * 128 + r;
+                if (scale) scale[sidx] = row_ok ? static_cast<float>(gg.step) : 0.0f;
+                if (zero) zero[sidx] = row_ok ? gg.zero_f : 0.0f;
+                if (row_ok && step64) {
+                    step64[q.row * G + q.g] = gg.step;
+                    zero64[q.row * G + q.g] = gg.zero;
+                }
+            }
+            // Fast path: xf = (w - zero) * rcp(step) in fp32 (|error| < 1e-4 for
+            // |xf| <= 255); away from a tie (|xf - rint(xf)| <=
+            // 0.5 - margin) floor(x + 0.5) == rint(xf) and lies in [lo, hi].
+            // Near ties / non-finite values take quant_code_exact. A flat
+            // group (step 0) has rcp 0: every code is 0, as the reference.
+            const float zf = gg.zero_f;
+            const float rf = gg.step == 0.0 ? 0.0f : gg.rcp_f;
+            using SP = slice_pack<BITS>;
+            uint32_t words[SP::NW];
+            SP::init_words(words, sym != 0);
+            uint32_t code15[2] = {0u, 0u};  // 3-bit pair 15 (codes 30, 31)
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+                const float x = elem(e);
+                const float xf = (x - zf) * rf;
+                const float nm = xf + kMagicF;
+                const float d = xf - (nm - kMagicF);
+                uint32_t bits = __float_as_uint(nm);
+                if (e >= q.valid) {
+                    bits = kMagicBits;  // padding: signed code 0
+                } else if (!(fabsf(d) <= 0.5f - kTieMargin && fabsf(xf) < 4096.0f)) {
+                    bits = kMagicBits + static_cast<uint32_t>(
+                                            quant_code_exact(x, gg.step, gg.zero, gg.lo, gg.hi));
+                }
+                if (SP::split3(e)) {
+                    code15[e & 1] = bits - kMagicBits + static_cast<uint32_t>(off);
+                } else {
+                    words[SP::word_of(e)] += bits << SP::shift_of(e);
+                }
+            }
+            if constexpr (BITS == 3) {
+                // pair 15: bit b of code 30 at bit 15, of code 31 at bit 31, of chunk b
+#pragma unroll
+                for (int b2 = 0; b2 < 3; ++b2)
+                    words[b2 * 4] |= (((code15[0] >> b2) & 1u) << 15) | (((code15[1] >> b2) & 1u) << 31);
+            }
+            if constexpr (BITS == 4) {
+                *reinterpret_cast<uint4*>(tbase + sl * 2048) = make_uint4(words[0], words[1], words[2], words[3]);
+            } else if constexpr (BITS == 8) {
+                *reinterpret_cast<uint4*>(tbase + (2 * sl) * 2048) = make_uint4(words[0], words[1], words[2], words[3]);
+                *reinterpret_cast<uint4*>(tbase + (2 * sl + 1) * 2048) = make_uint4(words[4], words[5], words[6], words[7]);
+            } else {
+#pragma unroll
+                for (int b2 = 0; b2 < 3; ++b2) *reinterpret_cast<uint32_t*>(tbase + b2 * 2048 + sl * 4) = words[b2 * 4];
+            }
         }
     }
+    cp_async_wait<0>();
 }
 
 // Unpack to row-major stored codes (u8, or raw bf16 words for 16-bit) and
@@ -270,14 +379,21 @@ cudaError_t launch_quant_pack(const void* w, int64_t n_out, int64_t k_in,
                               double* zero64, cudaStream_t st) {
     const int G = static_cast<int>(ceil_div64(k_in, 128));
     // rows up to the 128-row tile boundary: padding rows get code 0 / scale 0
-    const dim3 grid(G, static_cast<unsigned>(ceil_div64(n_out, 128) * (128 / kQRows)));
+    const int64_t items = ceil_div64(n_out, 128) * (128 / kQRows) * G;
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const unsigned grid = static_cast<unsigned>(items < 3LL * sms ? items : 3LL * sms);
     auto* wp = static_cast<const __nv_bfloat16*>(w);
     auto* pp = static_cast<uint8_t*>(packed);
     switch (bits) {
-        case 3: quant_pack_kernel<3><<<grid, 256, 0, st>>>(wp, n_out, k_in, ldw, G, sym, pp, scale, zero, step64, zero64); break;
-        case 4: quant_pack_kernel<4><<<grid, 256, 0, st>>>(wp, n_out, k_in, ldw, G, sym, pp, scale, zero, step64, zero64); break;
-        case 8: quant_pack_kernel<8><<<grid, 256, 0, st>>>(wp, n_out, k_in, ldw, G, sym, pp, scale, zero, step64, zero64); break;
-        case 16: quant_pack_kernel<16><<<grid, 256, 0, st>>>(wp, n_out, k_in, ldw, G, sym, pp, scale, zero, step64, zero64); break;
+        case 3: quant_pack_kernel<3><<<grid, 256, 0, st>>>(wp, n_out, k_in, ldw, G, sym, items, pp, scale, zero, step64, zero64); break;
+        case 4: quant_pack_kernel<4><<<grid, 256, 0, st>>>(wp, n_out, k_in, ldw, G, sym, items, pp, scale, zero, step64, zero64); break;
+        case 8: quant_pack_kernel<8><<<grid, 256, 0, st>>>(wp, n_out, k_in, ldw, G, sym, items, pp, scale, zero, step64, zero64); break;
+        case 16: quant_pack_kernel<16><<<grid, 256, 0, st>>>(wp, n_out, k_in, ldw, G, sym, items, pp, scale, zero, step64, zero64); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

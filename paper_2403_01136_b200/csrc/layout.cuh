@@ -59,7 +59,7 @@ struct code_pos {
     int chunk2, word2, shift2; // 3-bit high bit plane
 };
 
-__host__ __device__ __forceinline__ code_pos locate_code(int bits, int kk) {
+__host__ __device__ __forceinline__ constexpr code_pos locate_code(int bits, int kk) {
     code_pos p{0, 0, 0, 0, 0, 0};
     const int pair = (kk >> 1), hi = kk & 1;
     if (bits == 4) {
