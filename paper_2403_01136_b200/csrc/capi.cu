@@ -290,7 +290,7 @@ hp_status hp_indicator_stats(const void* w, int64_t n_out, int64_t k_in, int64_t
         return fail(HP_EINVAL, "indicator_stats: bad calibration shape");
     if (hp_status s = need_device()) return s;
     auto st = static_cast<cudaStream_t>(stream);
-    // ~8 blocks of 256 threads per SM, split between W and X by bytes
+    // 3 resident blocks of 256 threads per SM (one wave), split between W and X by cost
     int sms = 148;
     {
         int dev = 0;
@@ -300,7 +300,7 @@ hp_status hp_indicator_stats(const void* w, int64_t n_out, int64_t k_in, int64_t
     // (an X element costs ~4x a W element: fp64 moments vs fp32 min/max, so
     // X blocks get proportionally fewer bytes and finish with the W blocks)
     const double wb = static_cast<double>(n_out) * k_in, xb = x ? 4.0 * tokens * k_in : 0.0;
-    const int nb = 8 * sms;
+    const int nb = 3 * sms;
     const int nbx = x ? std::max(1, std::min(nb - 1, static_cast<int>(nb * xb / (wb + xb)))) : 0;
     const int nbw = std::max(1, nb - nbx);
     const size_t bytes = hp::stats_scratch_bytes(nbw, nbx);

@@ -17,6 +17,7 @@
 // weights take the slow path.
 #include <cuda_bf16.h>
 #include <cstdint>
+#include <type_traits>
 #include <utility>
 
 #include "layout.cuh"
@@ -142,11 +143,11 @@ __global__ void __launch_bounds__(256, 3)
         int g, valid;
         bool full;
     };
-    auto locate = [&](int64_t it) {
+    auto locate = [&](int64_t it) {  // items < 2^31 (BLOOM fc1: 100k)
         where q;
-        const int64_t rb = it / G;
-        q.g = static_cast<int>(it - rb * G);
-        q.row = rb * kQRows + rin;
+        const uint32_t rb = static_cast<uint32_t>(it) / static_cast<uint32_t>(G);
+        q.g = static_cast<int>(static_cast<uint32_t>(it) - rb * static_cast<uint32_t>(G));
+        q.row = static_cast<int64_t>(rb) * kQRows + rin;
         q.k0 = static_cast<int64_t>(q.g) * 128 + sl * 32;
         const int cnt = static_cast<int>(k_in - q.k0 <= 0 ? 0 : (k_in - q.k0 < 32 ? k_in - q.k0 : 32));
         q.valid = q.row < n_out ? cnt : 0;
@@ -245,33 +246,74 @@ __global__ void __launch_bounds__(256, 3)
                 }
             }
             // Fast path: xf = (w - zero) * rcp(step) in fp32 (|error| < 1e-4 for
-            // |xf| <= 255); away from a tie (|xf - rint(xf)| <=
-            // 0.5 - margin) floor(x + 0.5) == rint(xf) and lies in [lo, hi].
+            // |xf| <= 255; |xf| <= hi by construction); away
+            // from a tie (|xf - rint(xf)| <= 0.5 - margin) floor(x + 0.5) ==
+            // rint(xf) and lies in [lo, hi].
             // Near ties / non-finite values take quant_code_exact. A flat
             // group (step 0) has rcp 0: every code is 0, as the reference.
             const float zf = gg.zero_f;
-            const float rf = gg.step == 0.0 ? 0.0f : gg.rcp_f;
+            // a step below FLT_MIN is a denormal float: rcp would be inexact,
+            // so NaN flags every code for the exact path
+            const float rf = gg.step == 0.0 ? 0.0f : (gg.step < 1.1754943508222875e-38 ? __int_as_float(0x7fc00000) : gg.rcp_f);
             using SP = slice_pack<BITS>;
             uint32_t words[SP::NW];
             SP::init_words(words, sym != 0);
             uint32_t code15[2] = {0u, 0u};  // 3-bit pair 15 (codes 30, 31)
+            // phase 1, branch-free (full ILP across the 32 codes): fast codes
+            // packed, near-tie / non-finite codes flagged in `slow`
+            // __fmul_rn/__fadd_rn: no FMA contraction, so phase 2 recomputes the
+            // very bits phase 1 packed
+            auto fast_bits = [&](float x) { return __float_as_uint(__fadd_rn(__fmul_rn(__fsub_rn(x, zf), rf), kMagicF)); };
+            uint32_t slow = 0;
+            auto phase1 = [&](auto full) {
+                constexpr bool kFull = decltype(full)::value;  // all 32 codes valid
 #pragma unroll
-            for (int e = 0; e < 32; ++e) {
-                const float x = elem(e);
-                const float xf = (x - zf) * rf;
-                const float nm = xf + kMagicF;
-                const float d = xf - (nm - kMagicF);
-                uint32_t bits = __float_as_uint(nm);
-                if (e >= q.valid) {
-                    bits = kMagicBits;  // padding: signed code 0
-                } else if (!(fabsf(d) <= 0.5f - kTieMargin && fabsf(xf) < 4096.0f)) {
-                    bits = kMagicBits + static_cast<uint32_t>(
-                                            quant_code_exact(x, gg.step, gg.zero, gg.lo, gg.hi));
+                for (int e = 0; e < 32; ++e) {
+                    const float x = elem(e);
+                    const float xf = __fmul_rn(__fsub_rn(x, zf), rf);
+                    const float nm = __fadd_rn(xf, kMagicF);
+                    const float d = xf - (nm - kMagicF);  // NaN for non-finite xf
+                    uint32_t bits = __float_as_uint(nm);
+                    const uint32_t flag = fabsf(d) <= 0.5f - kTieMargin ? 0u : (1u << e);
+                    if (!kFull && e >= q.valid) {
+                        bits = kMagicBits;  // padding: signed code 0
+                    } else {
+                        slow |= flag;
+                    }
+                    if (SP::split3(e)) {
+                        code15[e & 1] = bits - kMagicBits + static_cast<uint32_t>(off);
+                    } else {
+                        words[SP::word_of(e)] += bits << SP::shift_of(e);
+                    }
                 }
-                if (SP::split3(e)) {
-                    code15[e & 1] = bits - kMagicBits + static_cast<uint32_t>(off);
+            };
+            if (q.full)
+                phase1(std::true_type{});
+            else
+                phase1(std::false_type{});
+            // phase 2 (~0.3% of codes): the exact fp64 code replaces the fast
+            // one. A rolled loop over the flagged codes (one copy of the fp64
+            // sequence keeps the kernel small); registers are selected, not
+            // indexed, so nothing goes to local memory.
+            while (slow) {
+                const int e = __ffs(slow) - 1;
+                slow &= slow - 1;
+                uint32_t vw = v[0];
+#pragma unroll
+                for (int i = 1; i < 16; ++i) vw = (i == (e >> 1)) ? v[i] : vw;
+                const float x = __uint_as_float((e & 1) ? (vw & 0xFFFF0000u) : (vw << 16));
+                const uint32_t ex = kMagicBits + static_cast<uint32_t>(
+                                                     quant_code_exact(x, gg.step, gg.zero, gg.lo, gg.hi));
+                if (BITS == 3 && ((e >> 1) & 15) == 15) {
+                    const uint32_t c = ex - kMagicBits + static_cast<uint32_t>(off);
+                    code15[0] = (e & 1) ? code15[0] : c;
+                    code15[1] = (e & 1) ? c : code15[1];
                 } else {
-                    words[SP::word_of(e)] += bits << SP::shift_of(e);
+                    const code_pos cp = locate_code(BITS, e);
+                    const int wi = cp.chunk * 4 + cp.word;
+                    const uint32_t delta = (ex - fast_bits(x)) << cp.shift;
+#pragma unroll
+                    for (int i = 0; i < SP::NW; ++i) words[i] += (i == wi) ? delta : 0u;
                 }
             }
             if constexpr (BITS == 3) {

@@ -8,7 +8,7 @@
 // host library in the reference's operation order.
 //
 // Both reductions are single-pass, HBM-bound and deterministic: every thread
-// streams 16-byte vectors (4 loads in flight) from an even contiguous share
+// streams 16-byte vectors (8 loads in flight) from an even contiguous share
 // of the tensor and folds them (min/max; for the moments each bf16x8 vector
 // becomes an exact fp64 (8, mean, M2) and is Chan-merged, one fp64 division
 // per 8 elements), blocks fold their threads in a fixed shuffle-tree order,
@@ -94,7 +94,7 @@ __device__ __forceinline__ T block_fold(T v, F op, T* sm) {
 
 // Rows [r0, r1) x k of a row-major bf16 matrix with leading dimension ld, as
 // bf16x8 vectors when rows are 16-byte aligned and contiguous (ld == k) or
-// padded to a multiple of 8; 4 independent 16-byte loads in flight per thread.
+// padded to a multiple of 8; 8 independent 16-byte loads in flight per thread.
 template <class V, class S>
 __device__ __forceinline__ void walk(const __nv_bfloat16* __restrict__ p, int64_t rows, int64_t k,
                                      int64_t ld, int part, int nparts, V vec_fn, S scalar_fn) {
@@ -105,12 +105,13 @@ __device__ __forceinline__ void walk(const __nv_bfloat16* __restrict__ p, int64_
         const int64_t lo = nvec * part / nparts, hi = nvec * (part + 1) / nparts;
         const uint4* v4 = reinterpret_cast<const uint4*>(p);
         int64_t i = lo + tid;
-        for (; i + 3 * kStatThreads < hi; i += 4 * kStatThreads) {
-            uint4 q[4];
+        constexpr int U = 8;  // 128 bytes in flight per thread
+        for (; i + (U - 1) * kStatThreads < hi; i += U * kStatThreads) {
+            uint4 q[U];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) q[u] = __ldcs(v4 + i + u * kStatThreads);
+            for (int u = 0; u < U; ++u) q[u] = __ldcs(v4 + i + u * kStatThreads);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) vec_fn(q[u]);
+            for (int u = 0; u < U; ++u) vec_fn(q[u]);
         }
         for (; i < hi; i += kStatThreads) vec_fn(__ldcs(v4 + i));
     } else if (aligned) {  // padded rows: parts take whole rows
@@ -126,7 +127,7 @@ __device__ __forceinline__ void walk(const __nv_bfloat16* __restrict__ p, int64_
 }
 
 // grid.x blocks: [0, nbw) reduce W (min/max), [nbw, nbw+nbx) reduce X.
-__global__ void __launch_bounds__(kStatThreads)
+__global__ void __launch_bounds__(kStatThreads, 3)
     stats_kernel(const __nv_bfloat16* __restrict__ w, int64_t n_out,
                  int64_t k_in, int64_t ldw, const __nv_bfloat16* __restrict__ x,
                  int64_t tokens, int64_t ldx, int nbw, int nbx,
