@@ -191,6 +191,8 @@ def main():
     ap.add_argument("--plan", default=None, help="override plan fixture name")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graphs", action="store_true")
+    ap.add_argument("--sm-budget", type=int, default=None,
+                    help="persistent-kernel grid cap (default: all SMs at N=1, 140 at N>1)")
     ap.add_argument("--decode-fused", action="store_true",
                     help="decode units as one K3-fused launch per bit-width run (hp_decode_plan)")
     args = ap.parse_args()
@@ -224,7 +226,8 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         ids = obj[0]
     pipe = Pipeline(plan_json, model_json, rank, world, ids, use_graphs=not args.no_graphs,
-                    instrument=True, sm_budget=140 if world > 1 else 0,
+                    instrument=True,
+                    sm_budget=args.sm_budget if args.sm_budget is not None else (140 if world > 1 else 0),
                     decode_fused=args.decode_fused)
     info = pipe.info()
     h1 = {"opt-13b": 5120, "opt-30b": 7168, "opt-66b": 9216, "bloom-176b": 14336}.get(

@@ -245,6 +245,16 @@ struct pipeline::impl {
         if (opt.sm_budget > 0) hp_set_sm_budget(opt.sm_budget);
 
         if (world > 1) {
+            // NCCL's send/recv kernels occupy their SMs (one CTA per channel)
+            // for as long as a message is outstanding -- a posted receive
+            // spins through the whole previous stage's unit. With NCCL's
+            // default P2P channel count they took enough SMs that the
+            // persistent 1-CTA-per-SM K3/K4 grids ran partly serialised
+            // (OPT-13B 2-stage bench: K4 786 TF/s, 36.3k tok/s). Two
+            // channels per link move the 21 MB prefill messages in well
+            // under a unit and leave the grid its SMs (K4 1208 TF/s, 52.7k
+            // tok/s). The caller's own setting wins.
+            setenv("NCCL_MAX_P2P_NCHANNELS", "2", 0);
             // link l: rank l -> rank (l+1) % world; ids[l] names link l
             nccl_ok(ncclGroupStart(), "group");
             const int prev = (rank - 1 + world) % world;
