@@ -212,6 +212,9 @@ def main():
 
     torch.cuda.set_device(local)
     if world > 1:
+        # before NCCL's first initialisation in this process (it caches its
+        # parameters): 2 P2P channels per link, see pipeline.cpp build()
+        os.environ.setdefault("NCCL_MAX_P2P_NCHANNELS", "2")
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     name = args.plan or PLAN_FOR_N.get(world)
@@ -262,6 +265,12 @@ def main():
         barrier()
     torch.cuda.profiler.stop()
     k1 = [pipe.kernel_stats(0), pipe.kernel_stats(1)]
+    if os.environ.get("HP_BENCH_PER_RANK"):  # diagnostics: every rank's instrumented units
+        for ph in (0, 1):
+            d = {k: k1[ph][k] - k0[ph][k] for k in k1[ph]}
+            print(f"[rank {rank}] phase {ph}: {d['launches']} launches, avg "
+                  f"{d['seconds'] / max(d['launches'], 1) * 1e6:.1f} us, stage cost {pipe.stage_cost()}",
+                  file=sys.stderr, flush=True)
     step_s = max_over_ranks(statistics.mean(times))
     pre_busy = max_over_ranks(statistics.mean(pre_s))
     dec_busy = max_over_ranks(statistics.mean(dec_s))

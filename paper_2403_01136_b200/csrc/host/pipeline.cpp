@@ -253,7 +253,10 @@ struct pipeline::impl {
             // (OPT-13B 2-stage bench: K4 786 TF/s, 36.3k tok/s). Two
             // channels per link move the 21 MB prefill messages in well
             // under a unit and leave the grid its SMs (K4 1208 TF/s, 52.7k
-            // tok/s). The caller's own setting wins.
+            // tok/s; 4 stages 70k -> 99.5k). The caller's own setting wins.
+            // NCCL caches its parameters at its first initialisation in the
+            // process, so a host that initialised NCCL before (torch.distributed
+            // with the nccl backend) must export it itself (bench.py does).
             setenv("NCCL_MAX_P2P_NCHANNELS", "2", 0);
             // link l: rank l -> rank (l+1) % world; ids[l] names link l
             nccl_ok(ncclGroupStart(), "group");

@@ -8,11 +8,17 @@ from __future__ import annotations
 
 import ctypes as C
 import json
+import os
 from dataclasses import dataclass
 from pathlib import Path
 
 from . import capi
 from .capi import check, lib
+
+# NCCL caches its parameters when it first initialises in the process: set
+# the executor's P2P channel cap (pipeline.cpp build()) before anything --
+# e.g. torch.distributed with the nccl backend -- creates a communicator.
+os.environ.setdefault("NCCL_MAX_P2P_NCHANNELS", "2")
 
 ROOT = Path(__file__).resolve().parents[1]
 PLANS = ROOT / "tests" / "golden" / "plans"
