@@ -245,6 +245,14 @@ hp_status hp_host_plan_check(const char* plan_json, char* out, int64_t cap);
  * token) triples into out3[3*cap]; *n = count.                          */
 hp_status hp_host_unit_order(const char* plan_json, const char* model_json, int stage,
                              int* out3, int cap, int* n);
+/* Latency model (hetplan::latcost, latcost.cpp:140-225; Eigen-free QR):
+ * fit a profile CSV "device,bit,phase,v,s,t,latency_s" into the model JSON
+ * (serialize_model, format_version 1) -> out[cap], *needed = bytes incl.
+ * the NUL (HP_EINVAL when cap is too small); predict phase 0 prefill(v, s)
+ * / 1 decode(v, s, t) from a model JSON.                                   */
+hp_status hp_host_latency_fit(const char* profile_csv, char* out, int64_t cap, int64_t* needed);
+hp_status hp_host_latency_predict(const char* model_json, const char* device, int bit, int phase,
+                                  double v, double s, double t, double* out);
 
 #ifdef __cplusplus
 }

@@ -95,6 +95,8 @@ def _load() -> C.CDLL:
         "hp_host_simulate": (i32, [P(d), i32, i32, i32, i32, i32, P(d), P(d), v, i64]),
         "hp_host_plan_check": (i32, [p, C.c_char_p, i64]),
         "hp_host_unit_order": (i32, [p, p, i32, P(i32), i32, P(i32)]),
+        "hp_host_latency_fit": (i32, [p, p, i64, P(i64)]),
+        "hp_host_latency_predict": (i32, [p, p, i32, i32, C.c_double, C.c_double, C.c_double, P(C.c_double)]),
     }
     sig.update({
         "hp_set_sm_budget": (None, [i32]),
@@ -132,7 +134,7 @@ EXPORTED = [
     "hp_quant_pack", "hp_quant_unpack", "hp_dequant", "hp_indicator_stats",
     "hp_qlinear_workspace_bytes", "hp_qlinear", "hp_host_scaling_factor", "hp_host_g_of_x",
     "hp_host_indicator_csv", "hp_host_omega_from_stats", "hp_host_memcost", "hp_host_preset",
-    "hp_host_make_schedule", "hp_host_simulate", "hp_host_plan_check", "hp_host_unit_order", "hp_set_sm_budget", "hp_set_pdl",
+    "hp_host_make_schedule", "hp_host_simulate", "hp_host_plan_check", "hp_host_unit_order", "hp_host_latency_fit", "hp_host_latency_predict", "hp_set_sm_budget", "hp_set_pdl",
     "hp_nccl_unique_id", "hp_pipeline_create", "hp_pipeline_run", "hp_pipeline_stage_costs",
     "hp_pipeline_kernel_stats", "hp_pipeline_layer_costs", "hp_pipeline_info", "hp_pipeline_destroy",
     "hp_layernorm", "hp_decode_plan_create", "hp_decode_plan_run", "hp_decode_plan_info", "hp_decode_plan_destroy",

@@ -10,6 +10,7 @@
 
 #include "hetplan/config.hpp"
 #include "hetplan/indicator/indicator.hpp"
+#include "hetplan/latcost/latcost.hpp"
 #include "hetplan/memcost/memcost.hpp"
 #include "hetplan/pipesim/pipesim.hpp"
 #include "hetplan/plan/plan_io.hpp"
@@ -206,6 +207,34 @@ hp_status hp_host_plan_check(const char* plan_json, char* out, int64_t cap) {
         const auto doc = hetplan::plan_io::parse_plan(plan_json);
         hetplan::plan_io::validate(doc);
         return put_string(hetplan::plan_io::serialize_plan(doc), out, cap);
+    } catch (const std::exception& e) {
+        return from_exception(e);
+    }
+}
+
+hp_status hp_host_latency_fit(const char* profile_csv, char* out, int64_t cap, int64_t* needed) {
+    try {
+        if (!profile_csv) throw std::invalid_argument("latency_fit: NULL profile");
+        const std::string js = hetplan::latcost::serialize_model(
+            hetplan::latcost::fit(hetplan::latcost::ingest_profile(profile_csv)));
+        if (needed) *needed = static_cast<int64_t>(js.size()) + 1;
+        if (!out || cap < static_cast<int64_t>(js.size()) + 1)
+            throw std::invalid_argument("latency_fit: output buffer too small");
+        std::memcpy(out, js.c_str(), js.size() + 1);
+        return HP_OK;
+    } catch (const std::exception& e) {
+        return from_exception(e);
+    }
+}
+
+hp_status hp_host_latency_predict(const char* model_json, const char* device, int bit, int phase,
+                                  double v, double s, double t, double* out) {
+    try {
+        if (!model_json || !device || !out) throw std::invalid_argument("latency_predict: NULL argument");
+        const auto m = hetplan::latcost::parse_model(model_json);
+        *out = phase == 0 ? hetplan::latcost::predict_prefill(m, device, bit, v, s)
+                          : hetplan::latcost::predict_decode(m, device, bit, v, s, t);
+        return HP_OK;
     } catch (const std::exception& e) {
         return from_exception(e);
     }

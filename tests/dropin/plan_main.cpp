@@ -1,9 +1,9 @@
 // Drop-in check (test-side): the reference's planner sources
 // (/root/reference/proj/src/optimizer_*.cpp), compiled UNCHANGED against the
-// B200 build's headers (include/hetplan/{types,config,memcost,indicator}.hpp)
-// and linked against libhetplan_b200.so, must produce the same plan as the
-// reference build. latcost (Eigen) is absent here; latcost_shim.cpp supplies
-// its two predict dot products from the header contract.
+// B200 build's headers (include/hetplan/{types,config,memcost,indicator,
+// latcost}.hpp) and linked against libhetplan_b200.so, must produce the same
+// plan as the reference build. latcost's predictions come from the build's
+// Eigen-free latcost.cpp (the reference's needs Eigen, absent here).
 #include <fstream>
 #include <iostream>
 #include <sstream>

@@ -1,6 +1,6 @@
 """Drop-in test: the reference's own planner sources compile
 UNCHANGED against include/hetplan/*.hpp of this build and link against
-libhetplan_b200.so (our re-implementation of types/config/memcost/indicator),
+libhetplan_b200.so (our re-implementation of types/config/memcost/indicator/latcost),
 and reproduce the reference planner's OPT-125M plan (proven optimal, so the
 result is machine-independent). CPU only; needs /root/reference (skipped on
 the GPU box, where it does not exist)."""
@@ -23,11 +23,12 @@ def test_reference_planner_links_against_b200_headers_and_library():
     assert lib.exists()
     srcs = [REF / "src" / f"{n}.cpp" for n in ("optimizer_instance", "optimizer_solver",
                                                "optimizer_enumeration", "optimizer_planner")]
-    srcs += [ROOT / "tests" / "dropin" / "plan_main.cpp", ROOT / "tests" / "dropin" / "latcost_shim.cpp"]
+    srcs += [ROOT / "tests" / "dropin" / "plan_main.cpp"]
     with tempfile.TemporaryDirectory() as td:
         exe = Path(td) / "plan_main"
-        # our headers FIRST: types/config/memcost/indicator resolve to this build;
-        # optimizer/* and latcost.hpp (not re-implemented) come from the reference
+        # our headers FIRST: types/config/memcost/indicator/latcost resolve to
+        # this build (latcost: the Eigen-free fit/predict in csrc/host/latcost.cpp);
+        # optimizer/* (not re-implemented) come from the reference
         cmd = ["/usr/bin/g++", "-std=c++20", "-O1", "-w", "-DFMT_HEADER_ONLY",
                f"-I{ROOT / 'include'}", f"-I{REF / 'include'}",
                f"-I{SITE / 'include/cudnn_frontend/thirdparty/nlohmann'}",
