@@ -13,6 +13,14 @@
 // index (types.hpp:80, checked by types.cpp:102). The loader keeps
 // device_order and layers as authoritative, sets stage.device = k, and only
 // checks device_index == device_order[k].
+// Format 2 is written by serialize_plan and adds what a
+// packed-weight artifact needs to be reproducible:
+//   "quant": {"group": 128, "scheme": "symmetric"|"asymmetric",
+//             "rounding": "nearest", "layout": "hp-tile-128x128-v1"}
+// and writes stages[k].device_index = k (the stage index stage_range::device
+// means), keeping the physical device in device_order[k]. Format-1 documents
+// (the reference CLI's, no "format_version" or 1) still load; they carry no
+// quant block and get the SPEC defaults (group 128, symmetric, nearest).
 
 #include <cstdint>
 #include <string>
@@ -22,7 +30,15 @@
 
 namespace hetplan::plan_io {
 
-inline constexpr int plan_format_version = 1;
+inline constexpr int plan_format_version = 2;
+inline constexpr const char* packed_layout_name = "hp-tile-128x128-v1";  // layout.cuh
+
+struct quant_spec {
+    int group = 128;     // K1/K3/K4 group size along k (the only one supported)
+    int scheme = 1;      // 0 asymmetric, 1 symmetric (hp_capi.h HP_ASYMMETRIC/HP_SYMMETRIC)
+    std::string rounding = "nearest";
+    std::string layout = packed_layout_name;
+};
 
 struct plan_document {
     plan p;
@@ -33,6 +49,9 @@ struct plan_document {
     workload load;
     std::vector<std::string> devices;  // names, in pipeline order
     std::uint64_t seed = 0;
+    int format_version = 1;  // as read; serialize_plan always writes 2
+    bool has_quant = false;  // document carried a "quant" block
+    quant_spec quant;
 };
 
 // std::invalid_argument on malformed JSON or missing fields.

@@ -843,6 +843,8 @@ pipeline::pipeline(const plan_io::plan_document& plan, const model_spec& model, 
         throw std::invalid_argument("pipeline: plan has " + std::to_string(plan.p.stages.size()) +
                                     " stages but world size is " + std::to_string(world));
     if (rank < 0 || rank >= world) throw std::invalid_argument("pipeline: bad rank");
+    if (plan.has_quant && plan.quant.scheme != opt.scheme)
+        throw std::invalid_argument("pipeline: the plan's quant.scheme differs from the options' scheme");
     if (model.num_layers != plan.num_layers)
         throw std::invalid_argument("pipeline: model/plan layer count mismatch");
     if (world > 1 && static_cast<int>(nccl_ids.size()) < world)

@@ -29,12 +29,35 @@ plan_document parse_plan(const std::string& json_text) {
         p.xi = j.at("xi").get<int>();
         p.device_order = j.at("device_order").get<std::vector<int>>();
         if (j.contains("devices")) d.devices = j.at("devices").get<std::vector<std::string>>();
+        d.format_version = j.value("format_version", 1);
+        if (d.format_version != 1 && d.format_version != 2)
+            reject("plan: unsupported format_version " + std::to_string(d.format_version));
+        if (j.contains("quant")) {
+            const json& q = j.at("quant");
+            d.has_quant = true;
+            d.quant.group = q.value("group", 128);
+            const std::string sch = q.value("scheme", std::string("symmetric"));
+            d.quant.rounding = q.value("rounding", std::string("nearest"));
+            d.quant.layout = q.value("layout", std::string(packed_layout_name));
+            if (d.quant.group != 128) reject("plan: quant.group must be 128 (the packed tile layout)");
+            if (sch != "symmetric" && sch != "asymmetric")
+                reject("plan: quant.scheme must be symmetric or asymmetric");
+            d.quant.scheme = sch == "symmetric" ? 1 : 0;
+            if (d.quant.rounding != "nearest") reject("plan: quant.rounding must be nearest");
+            if (d.quant.layout != packed_layout_name)
+                reject("plan: unknown packed layout '" + d.quant.layout + "'");
+        }
         const json& st = j.at("stages");
         for (size_t k = 0; k < st.size(); ++k) {
             const json& s = st[k];
             const int di = s.at("device_index").get<int>();
-            if (k < p.device_order.size() && di != p.device_order[k])
-                reject("plan: stages[" + std::to_string(k) + "].device_index != device_order");
+            // format 1 (reference CLI, hetplan_main.cpp:209): device_order[k];
+            // format 2: the stage index k
+            const int want = d.format_version >= 2 ? static_cast<int>(k)
+                                                   : (k < p.device_order.size() ? p.device_order[k] : di);
+            if (di != want)
+                reject("plan: stages[" + std::to_string(k) + "].device_index is " + std::to_string(di) +
+                       ", expected " + std::to_string(want));
             p.stages.push_back({static_cast<int>(k), s.at("layers").at(0).get<int>(),
                                 s.at("layers").at(1).get<int>()});
         }
@@ -68,7 +91,7 @@ std::string serialize_plan(const plan_document& d) {
     json stages = json::array();
     for (size_t k = 0; k < d.p.stages.size(); ++k) {
         json s;
-        s["device_index"] = k < d.p.device_order.size() ? d.p.device_order[k] : static_cast<int>(k);
+        s["device_index"] = static_cast<int>(k);  // format 2: the stage index
         if (k < d.devices.size()) s["device"] = d.devices[k];
         s["layers"] = {d.p.stages[k].begin, d.p.stages[k].end};
         stages.push_back(s);
@@ -82,6 +105,10 @@ std::string serialize_plan(const plan_document& d) {
                       {"total", o.total}};
     j["optimal"] = d.p.optimal;
     j["seed"] = d.seed;
+    j["quant"] = {{"group", d.quant.group},
+                  {"scheme", d.quant.scheme == 1 ? "symmetric" : "asymmetric"},
+                  {"rounding", d.quant.rounding},
+                  {"layout", d.quant.layout}};
     return j.dump(2) + "\n";
 }
 

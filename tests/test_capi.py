@@ -77,6 +77,36 @@ def test_plan_documents_round_trip_and_validate():
         capi.check(capi.lib.hp_host_plan_check(json.dumps(bad).encode(), buf, len(buf)))
 
 
+def test_plan_format_2_round_trip():
+    """Plan JSON v2: serialize writes format_version 2,
+    the quant block and device_index = stage index; v2 reloads to the same
+    plan; reference-format (v1) documents still load; bad quant rejected."""
+    import ctypes as C
+    import json
+    plans = Path(__file__).resolve().parent / "golden" / "plans"
+    for f in sorted(plans.glob("*gpu.json")):
+        buf = C.create_string_buffer(1 << 20)
+        capi.check(capi.lib.hp_host_plan_check(f.read_bytes(), buf, len(buf)))
+        v2 = json.loads(buf.value)
+        assert v2["format_version"] == 2
+        assert v2["quant"] == {"group": 128, "scheme": "symmetric", "rounding": "nearest",
+                               "layout": "hp-tile-128x128-v1"}
+        assert [s["device_index"] for s in v2["stages"]] == list(range(len(v2["stages"])))
+        buf2 = C.create_string_buffer(1 << 20)
+        capi.check(capi.lib.hp_host_plan_check(buf.value, buf2, len(buf2)))
+        assert json.loads(buf2.value) == v2  # fixed point
+    base = json.loads(buf.value)
+    for key, val in (("group", 64), ("scheme", "nf4"), ("rounding", "stochastic"), ("layout", "gptq")):
+        bad = json.loads(json.dumps(base))
+        bad["quant"][key] = val
+        with pytest.raises(capi.InvalidArgument):
+            capi.check(capi.lib.hp_host_plan_check(json.dumps(bad).encode(), buf2, len(buf2)))
+    bad = json.loads(json.dumps(base))
+    bad["format_version"] = 3
+    with pytest.raises(capi.InvalidArgument):
+        capi.check(capi.lib.hp_host_plan_check(json.dumps(bad).encode(), buf2, len(buf2)))
+
+
 def test_cpp_wrappers_keep_reference_exception_contract(tmp_path):
     """include/hetplan/{quant,qlinear}.hpp rethrow hp_status as the reference's
     exception types: invalid_argument / runtime_error."""
