@@ -466,24 +466,10 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
                 const int s = it % CR, as = it % AS;
                 const int trole = (lane == 0 && warp == 4) ? 2 : -1;
                 if (trole >= 0) trace_ev(a, trole, it, 0);
-                if constexpr (C::kRR) {
-                    // one warp of the warpgroup polls the two mbarriers, the
-                    // other three sleep on the warpgroup's named barrier: a
-                    // try_wait loop costs issue slots on every wake-up, and
-                    // the dequant warps are issue-bound
-                    if (lq == 0) {
-                        mbar_wait(&full_c[s], (it / CR) & 1);
-                        if (trole >= 0) trace_ev(a, trole, it, 1);
-                        mbar_wait(&aempty[as], ((it / AS) & 1) ^ 1);
-                        if (trole >= 0) trace_ev(a, trole, it, 2);
-                    }
-                    named_bar_sync<128>(3 + wg);
-                } else {
-                    mbar_wait(&full_c[s], (it / CR) & 1);
-                    if (trole >= 0) trace_ev(a, trole, it, 1);
-                    mbar_wait(&aempty[as], ((it / AS) & 1) ^ 1);
-                    if (trole >= 0) trace_ev(a, trole, it, 2);
-                }
+                mbar_wait(&full_c[s], (it / CR) & 1);
+                if (trole >= 0) trace_ev(a, trole, it, 1);
+                mbar_wait(&aempty[as], ((it / AS) & 1) ^ 1);
+                if (trole >= 0) trace_ev(a, trole, it, 2);
                 tc_fence_after();
                 const int x0 = kh * kSl;  // first local slice of this warp
                 const int gi = x0 >> 2;

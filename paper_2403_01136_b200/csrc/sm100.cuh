@@ -83,13 +83,6 @@ __device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
     }
 }
 
-// Named barrier over `count` threads (warp multiples); orders shared-memory
-// accesses across the participating warps like __syncthreads does.
-template <int COUNT>
-__device__ __forceinline__ void named_bar_sync(int id) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(COUNT) : "memory");
-}
-
 // ---- programmatic dependent launch ------------------------------------------
 // wait: block until the preceding grid in the stream completed and its memory
 // is visible; trigger: let the next grid start launching (its prologue and

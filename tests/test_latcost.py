@@ -118,3 +118,24 @@ def test_predict_and_clamp():
     assert predict(m, "b200", 4, 1, 32, 512, 50) == pytest.approx(want, rel=1e-15)
     out = C.c_double()
     assert lib.hp_host_latency_predict(json.dumps(m).encode(), b"b200", 8, 1, 1, 1, 1, C.byref(out)) != 0
+
+
+def test_b200_profile_fixture_refits_to_committed_model():
+    """tools/latency_profile.py on a B200 wrote the per-layer profile and its
+    fitted model (tests/golden/plans/b200_opt13b.*); refitting the committed
+    profile reproduces the committed model, and it predicts every profiled
+    decode point within its residual bound."""
+    from pathlib import Path
+    plans = Path(__file__).parent / "golden" / "plans"
+    csv = (plans / "b200_opt13b.profile.csv").read_text()
+    committed = json.loads((plans / "b200_opt13b.latency_model.json").read_text())
+    refit = fit(csv)
+    for a, b in zip(refit["groups"], committed["groups"]):
+        assert (a["device"], a["bit"], a["phase"]) == (b["device"], b["bit"], b["phase"])
+        assert np.allclose(a["coeffs"], b["coeffs"], rtol=1e-12, atol=1e-18)
+    for line in csv.strip().splitlines()[1:]:
+        dev, bit, ph, v, s, t, lat = line.split(",")
+        if ph == "decode":
+            g = next(g for g in committed["groups"] if g["bit"] == int(bit) and g["phase"] == "decode")
+            got = predict(committed, dev, int(bit), 1, float(v), float(s), float(t))
+            assert abs(got - float(lat)) <= g["residuals"]["max_abs"] * (1 + 1e-9) + 1e-15
