@@ -169,9 +169,11 @@ def run_reference(args, rank: int, world: int):
         if i >= args.warmup:
             vals.append(r)
     v = statistics.mean(x["value"] for x in vals)
+    B, s_, n = plan["workload"]["global_bz"], plan["workload"]["s"], plan["workload"]["n"]
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tok/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            # the CPU round time the sample extrapolates to (B*s + B*(n-1) tokens)
+            "ms_per_step": (B * s_ + B * (n - 1)) / v * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_name(name, world), "plan": name},
             "cpu_baseline": {"value": v, "unit": "tok/s", "cores": threads, "kind": "port",
