@@ -158,3 +158,18 @@ def test_shared_workspace_across_tile_counts(cuda):
     chained = qweight.qlinear(big, x, workspace=ws)
     torch.cuda.synchronize()
     assert torch.equal(fresh, chained)
+
+
+@pytest.mark.parametrize("bits", (3, 16))
+def test_prefill_many_token_tiles_ragged(cuda, bits):
+    """A long prefill (149 BN=256 token tiles, one more than the persistent
+    grid, the last one ragged) matches the oracle: every CTA walks several
+    tiles and the partial tile's rows are masked."""
+    from paper_2403_01136_b200 import qweight
+    rng = np.random.default_rng(4242 + bits)
+    n, k, m = 128, 256, 256 * 149 - 77
+    qw, x, xb, codes, s64, z64, _ = _case(rng, n, k, m, bits, 1, cuda)
+    y = qweight.qlinear(qw, x, phase=0)
+    got = bf16_bits_to_f64(torch_to_bits(y))
+    ref = _oracle(xb, codes, s64, z64, bits, 1).astype(np.float64)
+    assert _err(got, ref) <= TOL
