@@ -25,6 +25,7 @@
 // tensor-bound.
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cmath>
 #include <cstdint>
 #include <cstdlib>
 
@@ -541,7 +542,7 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
             mbar_wait(&tfull[acc], (ut / NACC) & 1);
             trace_ev(a, warp == C::kEpiWarp0 && lane == 0 ? 3 : 99, 48 + ut, 1);
             tc_fence_after();
-            constexpr bool kSK = BN <= 64;  // stream-K only runs the decode tiles
+            constexpr bool kSK = true;  // stream-K: decode tiles, and wave-quantised prefill ops
             // partials: [tile][seg][BN/4][128 rows] float4 -- row r is the
             // thread, so every warp access is 512 contiguous bytes
             float4* part = (kSK && sg.nseg > 1)
@@ -763,7 +764,17 @@ qgemm_plan plan_qgemm(int64_t n_out, int64_t k_in, int64_t m, int phase) {
     p.maxseg = 1;
     p.total = tiles * G;
     // stream-K when whole tiles would leave SMs idle or unbalanced
-    p.stream_k = (phase == 1 && tiles % sms != 0 && tiles <= static_cast<int64_t>(kTicketBytes / 4)) ? 1 : 0;
+    // stream-K when whole tiles would leave SMs idle: every decode op whose
+    // tile count is not a multiple of the grid, and prefill ops whose last
+    // wave is badly filled ([5120 x 5120] / [5120 x 20480] at 2048 tokens:
+    // 320 BN=256 tiles = 2.16 waves, 72% busy; their whole-tile K4 ran at
+    // 1.03 / 1.24 PF/s against 1.4 for the well-filled qkv / fc1)
+    const double waves = static_cast<double>(tiles) / sms;
+    const bool prefill_sk = phase == 0 && tiles > sms && waves / std::ceil(waves) < 0.85;
+    p.stream_k = ((phase == 1 && tiles % sms != 0) || prefill_sk) &&
+                         tiles <= static_cast<int64_t>(kTicketBytes / 4)
+                     ? 1
+                     : 0;
     if (p.stream_k) {
         p.grid = static_cast<int>(p.total < sms ? p.total : sms);
         const int64_t per = p.total / p.grid;  // >= 1 group-step per CTA
