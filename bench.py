@@ -326,10 +326,13 @@ def main():
                      "source": e["source"]} if e else None)
         pre_share = pre_busy / (pre_busy + dec_busy) if pre_busy + dec_busy > 0 else 0
         roof_pre = {"kernel": "K4 prefill dequant-GEMM (hp::qgemm_kernel, BN=256)",
-                    "bound": "tensor", "achieved": k4, "peak": tf_sus, "unit": "TFLOP/s",
-                    "frac": k4 / tf_sus if k4 else None, "traffic": traffic("k4"),
+                    # the burst peak: K4 inside the round already exceeds the
+                    # "sustained" cuBLAS figure, which is therefore no ceiling
+                    "bound": "tensor", "achieved": k4, "peak": tf_burst, "unit": "TFLOP/s",
+                    "frac": k4 / tf_burst if k4 else None, "frac_of_sustained": k4 / tf_sus if k4 else None,
+                    "traffic": traffic("k4"),
                     "traffic_capture": traffic_note("k4"),
-                    "peak_kind": f"{src} bf16_tflops_sustained (burst {tf_burst})",
+                    "peak_kind": f"{src} bf16_tflops burst (sustained {tf_sus})",
                     "per_launch": {"launches": d_pre["launches"],
                                    "avg_flops": d_pre["flops"] / max(d_pre["launches"], 1),
                                    "avg_s": d_pre["seconds"] / max(d_pre["launches"], 1)},
