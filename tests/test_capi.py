@@ -64,7 +64,7 @@ def test_plan_documents_round_trip_and_validate():
     import ctypes as C
     import json
     plans = Path(__file__).resolve().parent / "golden" / "plans"
-    for f in sorted(plans.glob("*gpu.json")):
+    for f in sorted([*plans.glob("*gpu.json"), *plans.glob("*gpu_weak.json")]):
         buf = C.create_string_buffer(1 << 20)
         capi.check(capi.lib.hp_host_plan_check(f.read_bytes(), buf, len(buf)))
         a, b = json.loads(f.read_text()), json.loads(buf.value)
@@ -84,7 +84,7 @@ def test_plan_format_2_round_trip():
     import ctypes as C
     import json
     plans = Path(__file__).resolve().parent / "golden" / "plans"
-    for f in sorted(plans.glob("*gpu.json")):
+    for f in sorted([*plans.glob("*gpu.json"), *plans.glob("*gpu_weak.json")]):
         buf = C.create_string_buffer(1 << 20)
         capi.check(capi.lib.hp_host_plan_check(f.read_bytes(), buf, len(buf)))
         v2 = json.loads(buf.value)
