@@ -80,7 +80,14 @@ __device__ __forceinline__ void trace_ev(const qgemm_args& a, int role, uint32_t
     }
 }
 
-// A work segment: groups [g0, g1) of output tile `tile` (= mt*NT + nt).
+// Tiles are numbered weight-major (tile = nt*MT + mt): the CTAs running at
+// the same time share weight row-tiles across token tiles, so a prefill
+// op streams each weight tile from HBM about once (the token tiles of x stay
+// L2-resident) instead of once per token tile. Decode has MT = 1.
+__device__ __forceinline__ int tile_mt(const qgemm_args& a, int tile) { return tile % a.MT; }
+__device__ __forceinline__ int tile_nt(const qgemm_args& a, int tile) { return tile / a.MT; }
+
+// A work segment: groups [g0, g1) of output tile `tile` (= nt*MT + mt).
 // Stream-K: CTA c owns group-steps [c*total/P, (c+1)*total/P) of the
 // tile-major order; a tile split over several CTAs is reduced by the last
 // one to finish, summing the partials in segment order (deterministic).
@@ -366,7 +373,7 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
         // ============ weight-code producer (whole warp, elected issue) ==========
         uint32_t it = 0;
         while (iter.next(a, sg)) {
-            const int nt = sg.tile % a.NT;
+            const int nt = tile_nt(a, sg.tile);
             for (int sl = 4 * sg.g0; sl < 4 * sg.g1; sl += SPS, ++it) {
                 const int g = sl >> 2;
                 const int ng = SPS >= 4 ? min(C::NG, sg.g1 - g) : 1;
@@ -406,7 +413,7 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
         pdl_wait();  // x is the previous kernel's output
         uint32_t it = 0;
         while (iter.next(a, sg)) {
-            const int mt = sg.tile / a.NT;
+            const int mt = tile_mt(a, sg.tile);
             for (int sl = 4 * sg.g0; sl < 4 * sg.g1; sl += SPS, ++it) {
                 const int s = it % BR;
                 mbar_wait_warp(&empty_b[s], ((it / BR) & 1) ^ 1);
@@ -536,7 +543,7 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
         const uint32_t lane_addr = static_cast<uint32_t>(lq * 32) << 16;
         uint32_t ut = 0;
         while (iter.next(a, sg)) {
-            const int mt = sg.tile / a.NT, nt = sg.tile % a.NT;
+            const int mt = tile_mt(a, sg.tile), nt = tile_nt(a, sg.tile);
             const int acc = ut % NACC;
             trace_ev(a, warp == C::kEpiWarp0 && lane == 0 ? 3 : 99, 48 + ut, 0);
             mbar_wait(&tfull[acc], (ut / NACC) & 1);
