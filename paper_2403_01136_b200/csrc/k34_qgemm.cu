@@ -35,6 +35,15 @@
 #ifndef HP_DEC_SPS
 #define HP_DEC_SPS 8
 #endif
+#ifndef HP_DWG
+#define HP_DWG 3
+#endif
+#ifndef HP_DEC_BR
+#define HP_DEC_BR 3
+#endif
+#ifndef HP_DEC_BUDGET_KB
+#define HP_DEC_BUDGET_KB 186
+#endif
 #ifndef HP_CR_CAP
 #define HP_CR_CAP 12
 #endif
@@ -164,7 +173,7 @@ struct qgemm_cfg {
     static constexpr int kMinBlocks = 1;
     static constexpr int kTmemCols = 512;
     static constexpr bool kRR = BN <= 64 && BITS != 16;
-    static constexpr int DWG = kRR ? 3 : 2;
+    static constexpr int DWG = kRR ? HP_DWG : 2;
     static constexpr int kThreads = 128 * (2 + DWG);
     static constexpr int kEpiWarp0 = 4 + 4 * DWG;
     static constexpr int NG = SPS >= 4 ? SPS / 4 : 1;            // groups touched per stage
@@ -176,8 +185,8 @@ struct qgemm_cfg {
     // Two rings: the weight-code ring (HBM latency, released as soon as the
     // dequant warps hold the codes in registers) is deep; the activation
     // ring (L2-resident x, released by the MMA) is shallow.
-    static constexpr int kBudget = 186 * 1024;
-    static constexpr int BR = BN <= 64 ? 3 : (BN <= 128 ? 6 : 4);
+    static constexpr int kBudget = (BN <= 64 ? HP_DEC_BUDGET_KB : 186) * 1024;
+    static constexpr int BR = BN <= 64 ? HP_DEC_BR : (BN <= 128 ? 6 : 4);
     static constexpr int CR_ = (kBudget - BR * kB) / kCS > HP_CR_CAP ? HP_CR_CAP : (kBudget - BR * kB) / kCS;
     // Round-robin consumers wait only on their own stages, so every ring slot
     // they consume must always belong to the same warpgroup (depth % DWG ==
