@@ -38,6 +38,12 @@
 #ifndef HP_DWG
 #define HP_DWG 3
 #endif
+// Group-scaled decode (sym 3/4/8-bit): dequant warps write the exact integer
+// codes, the MMA sums every 128-k group into its own TMEM accumulator and the
+// epilogue applies the fp32 group scale to the group sum.
+#ifndef HP_DEC_GS
+#define HP_DEC_GS 0
+#endif
 #ifndef HP_DEC_BR
 #define HP_DEC_BR 3
 #endif
@@ -193,7 +199,10 @@ struct qgemm_cfg {
     // 0); otherwise an mbarrier parity wait could alias another phase.
     static constexpr int CR = kRR ? (CR_ / DWG) * DWG : CR_;
     static constexpr int NACC = BN <= 128 ? 2 : 1;
-    static constexpr int A0_ = NACC * BN < 64 ? 64 : NACC * BN;
+    static constexpr bool kGSok = kRR && HP_DEC_GS;               // sym kernels only (see kernel)
+    static constexpr int GCOLS = kGSok ? 2 * NG * BN : 0;          // 2 stage slots x NG group sums
+    static constexpr int A0_ = NACC * BN < 64 ? (GCOLS > 64 ? GCOLS : 64)
+                                               : (NACC * BN > GCOLS ? NACC * BN : GCOLS);
     static constexpr int A0 = (A0_ + 63) / 64 * 64;
     static constexpr int ACOLS = 16 * SPS;                       // TMEM columns per A stage
     static constexpr int AS_ = (kTmemCols - A0) / ACOLS > 8 ? 8 : (kTmemCols - A0) / ACOLS;
@@ -308,6 +317,7 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
     qgemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const qgemm_args a) {
     using C = qgemm_cfg<BITS, BN, SPS>;
     constexpr int AS = C::AS, NACC = C::NACC;
+    constexpr bool GS = C::kGSok && SYM;  // group-scaled decode (tfull/tempty per stage slot)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -434,7 +444,32 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
         // ===================== MMA issuer (whole warp, elected issue) ==========
         constexpr uint32_t idesc = umma_idesc_bf16(128, BN);
         uint32_t it = 0, ut = 0;
-        while (iter.next(a, sg)) {
+        if constexpr (GS) {
+            // one accumulator per 128-k group, in stage slot it&1
+            while (iter.next(a, sg)) {
+                for (int sl = 4 * sg.g0; sl < 4 * sg.g1; sl += SPS, ++it) {
+                    const int nsl = min(SPS, 4 * sg.g1 - sl);
+                    const int s = it % BR, as = it % AS, slot = it & 1;
+                    mbar_wait_warp(&tempty[slot], ((it >> 1) & 1) ^ 1);
+                    mbar_wait_warp(&full_b[s], (it / BR) & 1);
+                    mbar_wait_warp(&afull[as], (it / AS) & 1);
+                    tc_fence_after();
+                    const uint32_t bbase = smem_u32(stage_b(s));
+                    const uint32_t abase = tmem + C::A0 + as * C::ACOLS;
+                    const uint64_t bdesc0 = umma_desc_sw128(bbase);
+#pragma unroll
+                    for (int q = 0; q < SPS / 2; ++q) {
+                        if (2 * q < nsl)
+                            mma_ts_x4_elect(tmem + (slot * C::NG + (q >> 1)) * BN, abase + q * 32,
+                                            bdesc0 + q * (BN * 8), idesc, (q & 1) ? 1u : 0u);
+                    }
+                    tc_commit_elect(&empty_b[s]);
+                    tc_commit_elect(&aempty[as]);
+                    tc_commit_elect(&tfull[slot]);
+                }
+            }
+        }
+        while (!GS && iter.next(a, sg)) {
             const int acc = ut % NACC;
             mbar_wait_warp(&tempty[acc], ((ut / NACC) & 1) ^ 1);
             tc_fence_after();
@@ -500,7 +535,7 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
                     sf[j] = 0.f;
                     zf[j] = 0.f;
                     if constexpr (BITS != 16) {
-                        if (4 * j + x0 < nsl) {
+                        if (!GS && 4 * j + x0 < nsl) {
                             const uint32_t saddr = smem_u32(stage_scale(s)) + ((gi + j) * 128 + r) * 4;
                             sf[j] = ldsf(saddr);
                             if constexpr (!SYM) zf[j] = ldsf(saddr + kScaleRow * 4);
@@ -530,8 +565,8 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
                     if (x0 + h < nsl) {
                         const int j = h >> 2;
                         uint32_t v[16];
-                        convert_slice<BITS, SYM>(wv[h], sf[j], zf[j], bf16x2_splat_bits(sf[j]),
-                                                 bf16x2_splat_bits(zf[j]), v);
+                        convert_slice<BITS, SYM, GS>(wv[h], sf[j], zf[j], bf16x2_splat_bits(sf[j]),
+                                                     bf16x2_splat_bits(zf[j]), v);
                         tmem_st16(tmem + lane_addr + C::A0 + as * C::ACOLS + (x0 + h) * 16, v);
                     }
                 }
@@ -550,15 +585,66 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
         const int lq = warp & 3;
         const int r = lq * 32 + lane;
         const uint32_t lane_addr = static_cast<uint32_t>(lq * 32) << 16;
-        uint32_t ut = 0;
+        uint32_t ut = 0, git = 0;
         while (iter.next(a, sg)) {
             const int mt = tile_mt(a, sg.tile), nt = tile_nt(a, sg.tile);
             const int acc = ut % NACC;
+            constexpr bool kSK = true;  // stream-K: decode tiles, and wave-quantised prefill ops
+            if constexpr (GS) {
+                // fold each stage's group sums into registers: acc += s_g * sum_g
+                float fa[BN];
+#pragma unroll
+                for (int i = 0; i < BN; ++i) fa[i] = 0.f;
+                for (int sl = 4 * sg.g0; sl < 4 * sg.g1; sl += SPS, ++git) {
+                    const int g = sl >> 2;
+                    const int ng = min(C::NG, sg.g1 - g);
+                    float sc[C::NG];
+#pragma unroll
+                    for (int j = 0; j < C::NG; ++j)
+                        sc[j] = j < ng ? __ldg(a.scale + (static_cast<size_t>(nt) * a.G + g + j) * 128 + r) : 0.f;
+                    const int slot = git & 1;
+                    mbar_wait(&tfull[slot], (git >> 1) & 1);
+                    tc_fence_after();
+#pragma unroll
+                    for (int j = 0; j < C::NG; ++j) {
+                        if (j < ng) {
+#pragma unroll
+                            for (int c0 = 0; c0 < BN; c0 += 16) {
+                                uint32_t v[16];
+                                tmem_ld16(tmem + lane_addr + (slot * C::NG + j) * BN + c0, v);
+                                tmem_ld_wait();
+#pragma unroll
+                                for (int i = 0; i < 16; ++i) fa[c0 + i] = fmaf(sc[j], __uint_as_float(v[i]), fa[c0 + i]);
+                            }
+                        }
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[slot]);
+                }
+                float4* part = sg.nseg > 1
+                                   ? reinterpret_cast<float4*>(a.partial) +
+                                         (static_cast<size_t>(sg.tile) * a.maxseg + sg.idx) * (BN / 4) * 128 + r
+                                   : nullptr;
+#pragma unroll
+                for (int c0 = 0; c0 < BN; c0 += 16) {
+                    if (part) {
+#pragma unroll
+                        for (int i = 0; i < 16; i += 4)
+                            __stcg(part + ((c0 + i) / 4) * 128,
+                                   make_float4(fa[c0 + i], fa[c0 + i + 1], fa[c0 + i + 2], fa[c0 + i + 3]));
+                    } else {
+                        float f[16];
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) f[i] = fa[c0 + i];
+                        stage_store16(a, stg, C::kStgLd, r, f, mt * BN + c0, nt * 128);
+                    }
+                }
+            } else {
             trace_ev(a, warp == C::kEpiWarp0 && lane == 0 ? 3 : 99, 48 + ut, 0);
             mbar_wait(&tfull[acc], (ut / NACC) & 1);
             trace_ev(a, warp == C::kEpiWarp0 && lane == 0 ? 3 : 99, 48 + ut, 1);
             tc_fence_after();
-            constexpr bool kSK = true;  // stream-K: decode tiles, and wave-quantised prefill ops
             // partials: [tile][seg][BN/4][128 rows] float4 -- row r is the
             // thread, so every warp access is 512 contiguous bytes
             float4* part = (kSK && sg.nseg > 1)
@@ -586,6 +672,7 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
+            }
             trace_ev(a, warp == C::kEpiWarp0 && lane == 0 ? 3 : 99, 48 + ut, 2);
 
             if constexpr (kSK) if (sg.nseg > 1) {

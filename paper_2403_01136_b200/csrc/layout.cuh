@@ -132,8 +132,9 @@ __device__ __forceinline__ uint32_t bf16x2_splat_bits(float f) {
     return d;
 }
 
-// (v - off) exactly, then * s (+ z): two bf16x2 FMAs.
-template <bool SYM>
+// (v - off) exactly, then * s (+ z): two bf16x2 FMAs. RAW: only the exact
+// integer (v - off); the group scale is applied to the fp32 group sum.
+template <bool SYM, bool RAW = false>
 __device__ __forceinline__ uint32_t finish_pair(uint32_t v, uint32_t negoff2,
                                                 uint32_t s2, uint32_t z2) {
 #ifdef HP_EXPERIMENT_RAW
@@ -142,6 +143,7 @@ __device__ __forceinline__ uint32_t finish_pair(uint32_t v, uint32_t negoff2,
     constexpr uint32_t one2 = 0x3F803F80u;  // bf16 1.0 x2
     uint32_t c;
     asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(c) : "r"(v), "r"(one2), "r"(negoff2));
+    if (RAW) return c;
     uint32_t d;
     if (SYM) {
         asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(c), "r"(s2), "r"(0x80008000u));
@@ -184,7 +186,7 @@ __device__ __forceinline__ void load_slice(uint32_t row_chunks, int slice,
     }
 }
 
-template <int BITS, bool SYM>
+template <int BITS, bool SYM, bool RAW = false>
 __device__ __forceinline__ void convert_slice(const slice_words<BITS>& in, float s, float z,
                                               uint32_t s2, uint32_t z2, uint32_t* out) {
     if constexpr (BITS == 4) {
@@ -193,7 +195,7 @@ __device__ __forceinline__ void convert_slice(const slice_words<BITS>& in, float
         for (int j = 0; j < 4; ++j)
 #pragma unroll
             for (int p = 0; p < 4; ++p)
-                out[4 * j + p] = finish_pair<SYM>(
+                out[4 * j + p] = finish_pair<SYM, RAW>(
                     lop3_and_or(in.w[j] >> (4 * p), 0x000F000Fu, kMagic128), negoff2, s2, z2);
     } else if constexpr (BITS == 3) {
         constexpr uint32_t negoff2 = SYM ? 0xC303C303u : 0xC300C300u;
@@ -201,11 +203,11 @@ __device__ __forceinline__ void convert_slice(const slice_words<BITS>& in, float
         for (int w = 0; w < 3; ++w)
 #pragma unroll
             for (int p = 0; p < 5; ++p)
-                out[5 * w + p] = finish_pair<SYM>(
+                out[5 * w + p] = finish_pair<SYM, RAW>(
                     lop3_and_or(in.w[w] >> (3 * p), 0x00070007u, kMagic128), negoff2, s2, z2);
         const uint32_t b01 = lop3_and_or(in.w[1] >> 14, 0x00020002u,
                                          lop3_and_or(in.w[0] >> 15, 0x00010001u, kMagic128));
-        out[15] = finish_pair<SYM>(lop3_and_or(in.w[2] >> 13, 0x00040004u, b01), negoff2, s2, z2);
+        out[15] = finish_pair<SYM, RAW>(lop3_and_or(in.w[2] >> 13, 0x00040004u, b01), negoff2, s2, z2);
     } else if constexpr (BITS == 8) {
         const float off = SYM ? 8388608.0f + 127.0f : 8388608.0f;
 #pragma unroll
@@ -214,8 +216,8 @@ __device__ __forceinline__ void convert_slice(const slice_words<BITS>& in, float
             for (int p = 0; p < 2; ++p) {
                 const float f0 = __uint_as_float(prmt(in.w[j], 0x4B000000u, 0x7540u + 2 * p)) - off;
                 const float f1 = __uint_as_float(prmt(in.w[j], 0x4B000000u, 0x7541u + 2 * p)) - off;
-                const float d0 = SYM ? f0 * s : __fmaf_rn(f0, s, z);
-                const float d1 = SYM ? f1 * s : __fmaf_rn(f1, s, z);
+                const float d0 = RAW ? f0 : (SYM ? f0 * s : __fmaf_rn(f0, s, z));
+                const float d1 = RAW ? f1 : (SYM ? f1 * s : __fmaf_rn(f1, s, z));
                 out[2 * j + p] = pack_bf16x2(d0, d1);
             }
     } else {
