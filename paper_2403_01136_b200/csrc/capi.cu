@@ -38,6 +38,7 @@ struct qgemm_plan {
     size_t workspace;
     int stream_k, maxseg;
     int64_t total;
+    int dp;
 };
 qgemm_plan plan_qgemm(int64_t n_out, int64_t k_in, int64_t m, int phase);
 struct dstage_op {

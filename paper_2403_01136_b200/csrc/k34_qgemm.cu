@@ -25,6 +25,7 @@
 // tensor-bound.
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -68,7 +69,8 @@ struct qgemm_args {
     int n_out, k_in, G, NT;
     int m, MT;
     int stream_k;       // 1: contiguous group ranges per CTA (decode), 0: whole tiles
-    int64_t total;      // MT*NT*G group-steps (stream-K)
+    int dp;             // stream-K: tiles [0, dp) run whole (data-parallel waves) first
+    int64_t total;      // (MT*NT - dp)*G group-steps (stream-K region)
     int maxseg;         // partial slots per tile (stream-K)
     __nv_bfloat16* y;
     int64_t ldy;
@@ -141,11 +143,15 @@ struct seg_iter {
         phase = 0;
     }
     __device__ __forceinline__ bool next(const qgemm_args& a, seg_t& s) {
-        if (!a.stream_k) {
-            if (u >= a.MT * a.NT) return false;
-            s = {u, 0, a.G, 0, 1};
-            u += gridDim.x;
-            return true;
+        if (!a.stream_k || u < a.dp) {
+            const int lim = a.stream_k ? a.dp : a.MT * a.NT;
+            if (u < lim) {
+                s = {u, 0, a.G, 0, 1};
+                u += gridDim.x;
+                return true;
+            }
+            if (!a.stream_k) return false;
+            u = lim;  // data-parallel waves done -> the stream-K region
         }
         if (phase == 0 && w >= w1) {  // last segment done -> the rest
             phase = 1;
@@ -153,13 +159,13 @@ struct seg_iter {
         }
         const int64_t lim = phase == 0 ? w1 : wlast;
         if (w >= lim) return false;
-        const int tile = static_cast<int>(w / a.G);
+        const int tile = static_cast<int>(w / a.G);  // within the stream-K region
         const int g0 = static_cast<int>(w % a.G);
         const int64_t tend = static_cast<int64_t>(tile + 1) * a.G;
         const int64_t wend = lim < tend ? lim : tend;
         const int first = sk_owner(static_cast<int64_t>(tile) * a.G, a.total, gridDim.x);
         const int last = sk_owner(tend - 1, a.total, gridDim.x);
-        s = {tile, g0, g0 + static_cast<int>(wend - w), static_cast<int>(blockIdx.x) - first,
+        s = {a.dp + tile, g0, g0 + static_cast<int>(wend - w), static_cast<int>(blockIdx.x) - first,
              last - first + 1};
         w = wend;
         return true;
@@ -191,7 +197,10 @@ struct qgemm_cfg {
     // Two rings: the weight-code ring (HBM latency, released as soon as the
     // dequant warps hold the codes in registers) is deep; the activation
     // ring (L2-resident x, released by the MMA) is shallow.
-    static constexpr int kBudget = (BN <= 64 ? HP_DEC_BUDGET_KB : 186) * 1024;
+#ifndef HP_PRE_BUDGET_KB
+#define HP_PRE_BUDGET_KB 186
+#endif
+    static constexpr int kBudget = (BN <= 64 ? HP_DEC_BUDGET_KB : HP_PRE_BUDGET_KB) * 1024;
     static constexpr int BR = BN <= 64 ? HP_DEC_BR : (BN <= 128 ? 6 : 4);
     static constexpr int CR_ = (kBudget - BR * kB) / kCS > HP_CR_CAP ? HP_CR_CAP : (kBudget - BR * kB) / kCS;
     // Round-robin consumers wait only on their own stages, so every ring slot
@@ -556,6 +565,7 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
                     }
                 }
                 // ... then hand the weight slot back to the producer at once
+                fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty_c[s]);
                 if (trole >= 0) trace_ev(a, 4, it, 0);
@@ -844,6 +854,7 @@ struct qgemm_plan {
     size_t workspace;
     int stream_k, maxseg;
     int64_t total;
+    int dp;  // stream-K: whole tiles [0, dp) first (data-parallel waves)
 };
 
 constexpr size_t kTicketBytes = 16384;  // stream-K tile tickets: <= 4096 tiles
@@ -878,6 +889,19 @@ qgemm_plan plan_qgemm(int64_t n_out, int64_t k_in, int64_t m, int phase) {
                          tiles <= static_cast<int64_t>(kTicketBytes / 4)
                      ? 1
                      : 0;
+    p.dp = 0;
+    if (p.stream_k && prefill_sk) {
+        // optional data-parallel + stream-K split: whole-tile waves first,
+        // the rest as stream-K. Measured slower on B200 than pure stream-K
+        // for the 2.16-wave ops (out 1.03-1.09 vs 1.10-1.19 PF/s, fc2 1.37-1.51
+        // vs 1.43-1.60), so 0 waves by default.
+        int dpw = 0;
+        if (const char* e = getenv("HP_PREFILL_DP_WAVES")) dpw = std::min(atoi(e), static_cast<int>(waves));
+        if (dpw > 0) {
+            p.dp = dpw * sms;
+            p.total = (tiles - p.dp) * G;
+        }
+    }
     if (p.stream_k) {
         p.grid = static_cast<int>(p.total < sms ? p.total : sms);
         const int64_t per = p.total / p.grid;  // >= 1 group-step per CTA
@@ -927,6 +951,7 @@ cudaError_t launch_qgemm(const CUtensorMap& map, const qgemm_plan& p, int bits,
     a.m = static_cast<int>(m);
     a.MT = p.mt;
     a.stream_k = p.stream_k;
+    a.dp = p.dp;
     a.total = p.total;
     a.maxseg = p.maxseg;
     a.y = static_cast<__nv_bfloat16*>(y);

@@ -473,6 +473,7 @@ __device__ __forceinline__ void dq_stage(uint32_t slot, int r, int nsl, uint32_t
             load_slice<BITS>(cbase, h, wv[h]);
         }
     }
+    fence_proxy_async_smem();  // ld.shared of the slot before its bulk-copy refill
     __syncwarp();
     if (lane == 0) mbar_arrive(empty_c);
 #pragma unroll

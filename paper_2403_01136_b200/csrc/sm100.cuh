@@ -235,6 +235,15 @@ __device__ __forceinline__ void tmem_st_wait() {
 __device__ __forceinline__ void tmem_ld_wait() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+// Generic-proxy shared-memory reads of a ring slot -> async-proxy refill
+// (cp.async.bulk / TMA) of the same slot: the WAR order across proxies
+// needs this fence before the slot is released. Without it a consumer's
+// ld.shared can still be in flight when the producer's bulk copy lands
+// (seen as a run-to-run race in 16-bit prefill stream-K, whose 3-deep code
+// ring turns slots over fastest).
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 // Each thread writes 16 consecutive 32-bit columns of its own lane.
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
     asm volatile(

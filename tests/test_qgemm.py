@@ -173,3 +173,27 @@ def test_prefill_many_token_tiles_ragged(cuda, bits):
     got = bf16_bits_to_f64(torch_to_bits(y))
     ref = _oracle(xb, codes, s64, z64, bits, 1).astype(np.float64)
     assert _err(got, ref) <= TOL
+
+
+@pytest.mark.parametrize("bits", (4, 16))
+def test_prefill_data_parallel_plus_stream_k(cuda, bits, monkeypatch):
+    """A wave-quantised prefill op (320 BN=256 tiles = 2.16 waves of 148
+    CTAs) runs its first wave as whole tiles and the rest as stream-K
+    group ranges when HP_PREFILL_DP_WAVES=1; both that split and the default
+    pure stream-K split match the oracle, and each is deterministic."""
+    import torch
+    from paper_2403_01136_b200 import qweight
+    rng = np.random.default_rng(777 + bits)
+    n, k, m = 5120, 512, 2048
+    qw, x, xb, codes, s64, z64, _ = _case(rng, n, k, m, bits, 1, cuda)
+    ref = _oracle(xb, codes, s64, z64, bits, 1).astype(np.float64)
+    for waves in (None, "1"):
+        if waves is None:
+            monkeypatch.delenv("HP_PREFILL_DP_WAVES", raising=False)
+        else:
+            monkeypatch.setenv("HP_PREFILL_DP_WAVES", waves)
+        y = qweight.qlinear(qw, x, phase=0)
+        for _ in range(5):  # the pre-fix cross-proxy race showed in ~1 of 6 calls
+            assert torch.equal(y, qweight.qlinear(qw, x, phase=0))
+        got = bf16_bits_to_f64(torch_to_bits(y))
+        assert _err(got, ref) <= TOL, waves
