@@ -45,14 +45,38 @@
 #ifndef HP_DEC_GS
 #define HP_DEC_GS 0
 #endif
+// Decode smem: a 6-deep activation ring inside a 218 KB budget (with the
+// MMA spin: 40-layer decode step 3013 -> 2959 us).
 #ifndef HP_DEC_BR
-#define HP_DEC_BR 3
+#define HP_DEC_BR 6
 #endif
 #ifndef HP_DEC_BUDGET_KB
-#define HP_DEC_BUDGET_KB 186
+#define HP_DEC_BUDGET_KB 218
 #endif
 #ifndef HP_CR_CAP
 #define HP_CR_CAP 12
+#endif
+
+// The MMA issuer is one latency-critical warp: it spins on its barriers
+// instead of suspending (40-layer decode step -0.7%; HP_MMA_SPIN=0 restores
+// the suspend hint).
+#ifndef HP_MMA_SPIN
+#define HP_MMA_SPIN 1
+#endif
+#if HP_MMA_SPIN
+#define MMA_WAIT mbar_wait_warp_spin
+#else
+#define MMA_WAIT mbar_wait_warp
+#endif
+#ifdef HP_PROD_SPIN
+#define PROD_WAIT mbar_wait_warp_spin
+#else
+#define PROD_WAIT mbar_wait_warp
+#endif
+#ifdef HP_DQ_SPIN
+#define DQ_WAIT mbar_wait_warp_spin
+#else
+#define DQ_WAIT mbar_wait
 #endif
 
 namespace hp {
@@ -407,7 +431,7 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
                 const int ng = SPS >= 4 ? min(C::NG, sg.g1 - g) : 1;
                 const int s = it % CR;
                 trace_ev(a, 0, it, 0);
-                mbar_wait_warp(&empty_c[s], ((it / CR) & 1) ^ 1);
+                PROD_WAIT(&empty_c[s], ((it / CR) & 1) ^ 1);
                 trace_ev(a, 0, it, 1);
                 const size_t t = static_cast<size_t>(nt) * a.G + g;
                 const uint8_t* gsrc = a.packed + t * (BITS * 2048);
@@ -444,7 +468,7 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
             const int mt = tile_mt(a, sg.tile);
             for (int sl = 4 * sg.g0; sl < 4 * sg.g1; sl += SPS, ++it) {
                 const int s = it % BR;
-                mbar_wait_warp(&empty_b[s], ((it / BR) & 1) ^ 1);
+                PROD_WAIT(&empty_b[s], ((it / BR) & 1) ^ 1);
                 mbar_arrive_expect_tx_elect(&full_b[s], static_cast<uint32_t>(C::kB));
                 tma_load_3d_elect(stage_b(s), &tmap_x, 0, mt * BN, sl >> 1, &full_b[s]);
             }
@@ -487,9 +511,9 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
                 const int nsl = min(SPS, 4 * sg.g1 - sl);
                 const int s = it % BR, as = it % AS;
                 trace_ev(a, 1, it, 0);
-                mbar_wait_warp(&full_b[s], (it / BR) & 1);
+                MMA_WAIT(&full_b[s], (it / BR) & 1);
                 trace_ev(a, 1, it, 1);
-                mbar_wait_warp(&afull[as], (it / AS) & 1);
+                MMA_WAIT(&afull[as], (it / AS) & 1);
                 trace_ev(a, 1, it, 2);
                 tc_fence_after();
                 const uint32_t bbase = smem_u32(stage_b(s));
@@ -527,9 +551,9 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
                 const int s = it % CR, as = it % AS;
                 const int trole = (lane == 0 && warp == 4) ? 2 : -1;
                 if (trole >= 0) trace_ev(a, trole, it, 0);
-                mbar_wait(&full_c[s], (it / CR) & 1);
+                DQ_WAIT(&full_c[s], (it / CR) & 1);
                 if (trole >= 0) trace_ev(a, trole, it, 1);
-                mbar_wait(&aempty[as], ((it / AS) & 1) ^ 1);
+                DQ_WAIT(&aempty[as], ((it / AS) & 1) ^ 1);
                 if (trole >= 0) trace_ev(a, trole, it, 2);
                 tc_fence_after();
                 const int x0 = kh * kSl;  // first local slice of this warp

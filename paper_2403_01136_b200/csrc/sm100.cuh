@@ -83,6 +83,21 @@ __device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
     }
 }
 
+// Same, spinning without the suspend hint (latency-critical single warps).
+__device__ __forceinline__ void mbar_wait_warp_spin(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    uint32_t done = 0;
+    while (!__all_sync(0xffffffffu, done)) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+    }
+}
+
 // ---- programmatic dependent launch ------------------------------------------
 // wait: block until the preceding grid in the stream completed and its memory
 // is visible; trigger: let the next grid start launching (its prologue and
