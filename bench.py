@@ -105,81 +105,63 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
-def cpu_sample(plan: dict, model_json: str, threads: int, budget_s: float = 20.0):
-    """Oracle-port CPU forward of one decoder layer (all 4 ops), decode at
-    m = xi and prefill at a 64-token chunk, extrapolated to the round."""
-    import numpy as np
-
-    import oracle
-    model = json.loads(model_json)
-    presets = {"opt-13b": (5120, 20480), "opt-30b": (7168, 28672), "opt-66b": (9216, 36864),
-               "bloom-176b": (14336, 57344)}
-    h1, h2 = presets[model["preset"]] if "preset" in model else (model["h1"], model["h2"])
-    L = plan["num_layers"]
-    B, s, n = plan["workload"]["global_bz"], plan["workload"]["s"], plan["workload"]["n"]
-    xi = plan["xi"]
-    bits = max(set(plan["layer_bits"]), key=plan["layer_bits"].count)
-    rng = np.random.default_rng(0)
-    port = oracle.port()
-    ops = []
-    for (nn, kk) in ((3 * h1, h1), (h1, h1), (h2, h1), (h1, h2)):
-        w = (rng.standard_normal((nn, kk), dtype=np.float32) * 0.02).view(np.uint32)
-        wb = (w >> 16).astype(np.uint16)
-        if bits == 16:
-            ops.append((wb, None, None, nn, kk))
-        else:
-            c, st, z = port.quantize_matrix(wb, bits, 1)
-            ops.append((c, st, z, nn, kk))
-
-    def layer(m):
-        x = (rng.standard_normal((m, h1), dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)
-        t0 = time.perf_counter()
-        for c, st, z, nn, kk in ops:
-            xin = x if kk == h1 else (rng.standard_normal((m, kk), dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)
-            port.qlinear(xin, c.view(np.uint16) if bits == 16 else c, st, z, bits, 1, threads)
-        return time.perf_counter() - t0
-
-    t_dec = layer(xi)
-    m_pre = 64
-    t_pre = layer(m_pre)
-    groups = -(-B // xi)
-    dec_round = groups * (n - 1) * L * t_dec
-    pre_round = (B * s / m_pre) * L * t_pre
-    tok = B * s + B * (n - 1)
-    return {"value": tok / (dec_round + pre_round), "unit": "tok/s", "cores": threads,
-            "sample": (f"oracle port (oracle/hp_oracle.c, fp64 dequant-GEMM, OpenMP) on one "
-                       f"{bits}-bit layer [h1={h1}, h2={h2}]: 4 ops at m={xi} (decode) and "
-                       f"m={m_pre} (prefill chunk), {t_dec + t_pre:.1f} s CPU wall, "
-                       f"extrapolated to {L} layers x B={B}, s={s}, n={n}"),
-            "decode_tok_s": B * (n - 1) / dec_round, "prefill_tok_s": B * s / pre_round}
+def cpu_baseline_line(plan_name: str, rank: int) -> dict:
+    """The CPU path timed on the host cores (oracle/cpu_baseline.py, which
+    imports nothing from the product): one measured bounded sample of this
+    workload (extrapolated, labelled), plus the single-thread reference
+    quantize() and build_indicator_table timings and the fully measured
+    OPT-125M configs[0] round."""
+    from oracle import cpu_baseline as cb
+    plan, model = cb.load_plan(plan_name)
+    smp = cb.SampleRound(plan, model)
+    r = smp.step()
+    return {"value": r["value"], "unit": "tok/s", "cores": smp.nthreads, "kind": "port",
+            "cpu_model": cb.cpu_model(), "sample": r["sample"], "sample_s": r["sample_s"],
+            "sample_gflop_s": r["sample_gflop_s"], "decode_tok_s": r["decode_tok_s"],
+            "prefill_tok_s": r["prefill_tok_s"], "generated_tok_s": r["generated_tok_s"],
+            "opt125m_full_round": cb.opt125m_full_round(smp.nthreads),
+            "ref_quantize_single_thread": cb.ref_quantize_rate(),
+            "ref_build_indicator_table": cb.ref_indicator_time(plan, model)}
 
 
 def run_reference(args, rank: int, world: int):
-    """--impl reference: the CPU path on the host cores, same metric/config."""
+    """--impl reference: the reference's CPU path on the host cores, same
+    metric/config as our arm. Only oracle/ is loaded (no product import).
+    A step is one bounded MEASURED sample of the workload (one layer per
+    distinct bit width at m = xi and a 128-token prefill chunk, ~seconds);
+    `value` extrapolates the sample's per-layer rates to the plan's round,
+    `ms_per_step` is the measured sample time."""
     if rank != 0:
         return
-    from paper_2403_01136_b200.pipeline import load_plan
+    from oracle import cpu_baseline as cb
     name = args.plan or PLAN_FOR_N.get(world, PLAN_FOR_N[1])
-    plan_json, model_json = load_plan(name)
-    plan = json.loads(plan_json)
-    threads = os.cpu_count() or 1
-    vals = []
+    plan, model = cb.load_plan(name)
+    smp = cb.SampleRound(plan, model)
+    vals, walls = [], []
     for i in range(args.warmup + args.steps):
-        r = cpu_sample(plan, model_json, threads)
+        r = smp.step()
         if i >= args.warmup:
             vals.append(r)
+            walls.append(r["sample_s"])
     v = statistics.mean(x["value"] for x in vals)
-    B, s_, n = plan["workload"]["global_bz"], plan["workload"]["s"], plan["workload"]["n"]
+    full = cb.opt125m_full_round(smp.nthreads)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tok/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            # the CPU round time the sample extrapolates to (B*s + B*(n-1) tokens)
-            "ms_per_step": (B * s_ + B * (n - 1)) / v * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "ms_per_step": statistics.mean(walls) * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp32 accumulate (bf16 x, dequant per indicator.cpp:53)",
+            "data": "synthetic",
             "config": {"workload": workload_name(name, world), "plan": name},
-            "cpu_baseline": {"value": v, "unit": "tok/s", "cores": threads, "kind": "port",
+            "decode_tok_s": statistics.mean(x["decode_tok_s"] for x in vals),
+            "prefill_tok_s": statistics.mean(x["prefill_tok_s"] for x in vals),
+            "generated_tok_s": statistics.mean(x["generated_tok_s"] for x in vals),
+            "cpu_baseline": {"value": v, "unit": "tok/s", "cores": smp.nthreads, "kind": "port",
+                             "cpu_model": cb.cpu_model(),
                              "sample": vals[0]["sample"] +
                              "; the reference implements no layer forward (SPEC.md:8), so its "
-                             "CPU path is the oracle port of indicator.cpp:53 dequant + GEMM"},
+                             "CPU path is the oracle restatement of indicator.cpp:53 dequant + GEMM"},
+            "opt125m_full_round": full,
+            "ref_quantize_single_thread": cb.ref_quantize_rate(),
+            "ref_build_indicator_table": cb.ref_indicator_time(plan, model),
             "e2e": {"value": v, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -351,7 +333,7 @@ def main():
         dominant, other = (roof_pre, roof_dec) if pre_share >= 0.5 else (roof_dec, roof_pre)
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            cpu = cpu_sample(plan, model_json, os.cpu_count() or 1)
+            cpu = cpu_baseline_line(name, rank)
         # pipesim on measured costs (comm estimated from payload / 770 GB/s)
         sim = None
         try:

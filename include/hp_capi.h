@@ -232,6 +232,11 @@ hp_status hp_host_indicator_csv(const char* stats_csv, const int* bits, int nbit
 hp_status hp_host_omega_from_stats(const double* stats5_per_op, int n_layers,
                                    int ops_per_layer, const int* bits, int nbits,
                                    int scheme, int rounding, double* omega_out);
+/* Monte-Carlo output variance of one operator row (indicator.cpp:231-284,
+ * SPEC Theorem 1 check): out4 = {total_var, extra_var, se_total, n}.      */
+hp_status hp_host_mc_output_variance(const double* w, int64_t d, double x_mean, double x_var,
+                                    int bit, int scheme, int rounding, int64_t n_samples,
+                                    uint64_t seed, double* out4);
 hp_status hp_host_memcost(const int64_t* model9, int bit, int64_t v, int64_t s,
                           int64_t n, int64_t* out3);
 hp_status hp_host_preset(const char* name, int64_t* model9);

@@ -24,8 +24,8 @@ def splitmix64(x: np.ndarray) -> np.ndarray:
         return z ^ (z >> np.uint64(31))
 
 
-def seed_for(*parts: int) -> int:
-    s = np.uint64(2403)
+def seed_for(*parts: int, base: int = 2403) -> int:
+    s = np.uint64(base)
     for p in parts:
         s = splitmix64(np.array([s ^ np.uint64(p)], dtype=np.uint64))[0]
     return int(s)

@@ -89,6 +89,7 @@ def _load() -> C.CDLL:
         "hp_host_g_of_x": (i32, [d, d, i32, P(d)]),
         "hp_host_indicator_csv": (i32, [p, P(i32), i32, i32, i32, C.c_char_p, i64]),
         "hp_host_omega_from_stats": (i32, [P(d), i32, i32, P(i32), i32, i32, i32, P(d)]),
+        "hp_host_mc_output_variance": (i32, [P(d), i64, d, d, i32, i32, i32, i64, C.c_uint64, P(d)]),
         "hp_host_memcost": (i32, [P(i64), i32, i64, i64, i64, P(i64)]),
         "hp_host_preset": (i32, [p, P(i64)]),
         "hp_host_make_schedule": (i32, [i32, i32, i32, P(i32), P(i32), P(i32), P(i32), i32]),
@@ -133,7 +134,7 @@ EXPORTED = [
     "hp_last_error", "hp_abi_version", "hp_device_ok", "hp_packed_bytes", "hp_scale_count",
     "hp_quant_pack", "hp_quant_unpack", "hp_dequant", "hp_indicator_stats",
     "hp_qlinear_workspace_bytes", "hp_qlinear", "hp_host_scaling_factor", "hp_host_g_of_x",
-    "hp_host_indicator_csv", "hp_host_omega_from_stats", "hp_host_memcost", "hp_host_preset",
+    "hp_host_indicator_csv", "hp_host_omega_from_stats", "hp_host_mc_output_variance", "hp_host_memcost", "hp_host_preset",
     "hp_host_make_schedule", "hp_host_simulate", "hp_host_plan_check", "hp_host_unit_order", "hp_host_latency_fit", "hp_host_latency_predict", "hp_set_sm_budget", "hp_set_pdl",
     "hp_nccl_unique_id", "hp_pipeline_create", "hp_pipeline_run", "hp_pipeline_stage_costs",
     "hp_pipeline_kernel_stats", "hp_pipeline_layer_costs", "hp_pipeline_info", "hp_pipeline_destroy",

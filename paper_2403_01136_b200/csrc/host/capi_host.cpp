@@ -124,6 +124,24 @@ hp_status hp_host_omega_from_stats(const double* stats5_per_op, int n_layers, in
     }
 }
 
+hp_status hp_host_mc_output_variance(const double* w, int64_t d, double x_mean, double x_var,
+                                    int bit, int scheme, int rounding, int64_t n_samples,
+                                    uint64_t seed, double* out4) {
+    try {
+        if (!w || !out4 || d <= 0) throw std::invalid_argument("mc: NULL/empty weights");
+        const auto r = hetplan::indicator::mc_output_variance(
+            std::vector<double>(w, w + d), x_mean, x_var, bit, qspec(scheme, rounding), n_samples,
+            seed);
+        out4[0] = r.total_var;
+        out4[1] = r.extra_var;
+        out4[2] = r.se_total;
+        out4[3] = static_cast<double>(r.n);
+        return HP_OK;
+    } catch (const std::exception& e) {
+        return from_exception(e);
+    }
+}
+
 hp_status hp_host_memcost(const int64_t* model9, int bit, int64_t v, int64_t s, int64_t n,
                           int64_t* out3) {
     try {

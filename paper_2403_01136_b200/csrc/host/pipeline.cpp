@@ -93,9 +93,10 @@ uint64_t splitmix(uint64_t z) {
     z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
     return z ^ (z >> 31);
 }
-// oracle/synth.py seed_for(*parts)
-uint64_t seed_for(std::initializer_list<uint64_t> parts) {
-    uint64_t s = 2403;
+// oracle/synth.py seed_for(*parts, base=...): the chain starts at the
+// options' seed (default 2403, the value the fixtures and tests use)
+uint64_t seed_for(uint64_t base, std::initializer_list<uint64_t> parts) {
+    uint64_t s = base;
     for (uint64_t p : parts) s = splitmix(s ^ p);
     return s;
 }
@@ -279,7 +280,7 @@ struct pipeline::impl {
             for (int o = 0; o < 4; ++o) {
                 opw& w = L.ops[o];
                 const int64_t nn = shp[o].n, kk = shp[o].k;
-                cuda_ok(hp::launch_synth(tmp, nn * kk, seed_for({1, uint64_t(l), uint64_t(o)}),
+                cuda_ok(hp::launch_synth(tmp, nn * kk, seed_for(opt.seed, {1, uint64_t(l), uint64_t(o)}),
                                          0.0, opt.weight_std, cs),
                         "synth weights");
                 const int64_t pb = hp_packed_bytes(nn, kk, L.bits);
@@ -301,7 +302,7 @@ struct pipeline::impl {
             }
             for (int j = 0; j < 4; ++j) {  // LN gain ~ 1, bias ~ 0 (synthetic)
                 L.ln[j] = alloc(h1 * 2);
-                cuda_ok(hp::launch_synth(L.ln[j], h1, seed_for({4, uint64_t(l), uint64_t(j)}),
+                cuda_ok(hp::launch_synth(L.ln[j], h1, seed_for(opt.seed, {4, uint64_t(l), uint64_t(j)}),
                                          (j % 2 == 0) ? 1.0 : 0.0, 0.02, cs),
                         "synth ln");
             }
@@ -314,7 +315,7 @@ struct pipeline::impl {
         prompt = alloc(static_cast<size_t>(B) * s * h1 * 2);
         if (rank == 0) {
             pristine = alloc(static_cast<size_t>(B) * s * h1 * 2);
-            cuda_ok(hp::launch_synth(pristine, int64_t(B) * s * h1, seed_for({3}), 0.0, 1.0, cs),
+            cuda_ok(hp::launch_synth(pristine, int64_t(B) * s * h1, seed_for(opt.seed, {3}), 0.0, 1.0, cs),
                     "synth prompt");
         }
         const int64_t Mx = std::max<int64_t>(M, xi);
@@ -327,12 +328,15 @@ struct pipeline::impl {
             if (world > 1 && rank == world - 1)
                 fb.push_back(alloc(static_cast<size_t>(group_size[g]) * h1 * 2));
         }
-        // split-K workspace: max over this stage's ops and both phases
-        for (const layer& L : layers)
-            for (const opw& w : L.ops)
-                for (int ph = 0; ph < 2; ++ph)
-                    ws_bytes = std::max(ws_bytes, hp_qlinear_workspace_bytes(
-                                                      &w.w, ph == 0 ? M : xi, ph));
+        // split-K workspace: max over this stage's ops and every (rows, phase)
+        // the round launches -- a ragged last prefill micro-batch (B % eta != 0)
+        // or a short last decode group can need MORE stream-K workspace than
+        // the full-size one (fewer tiles -> more segments per tile)
+        for (const auto& sh : round_shapes())
+            for (const layer& L : layers)
+                for (const opw& w : L.ops)
+                    ws_bytes = std::max(ws_bytes,
+                                        hp_qlinear_workspace_bytes(&w.w, sh.first, sh.second));
         if (ws_bytes) {
             ws = alloc(ws_bytes);
             cuda_ok(cudaMemsetAsync(ws, 0, ws_bytes, cs), "ws");
@@ -448,18 +452,24 @@ struct pipeline::impl {
     // waits for a message this very stage must first compute and send) it
     // never returns. So run every (phase, rows) forward the round will use,
     // plus the gather, once on scratch before any NCCL operation is posted.
-    void load_kernels() {
+    // every distinct (rows, phase) the round's units run with
+    std::vector<std::pair<int64_t, int>> round_shapes() const {
         std::vector<std::pair<int64_t, int>> shapes;
         for (int k = 0; k < static_cast<int>(sched.prefill_sizes.size()); ++k)
             shapes.push_back({prefill_rows(k), HP_PREFILL});
         for (int g = 0; g < sched.num_groups; ++g) shapes.push_back({group_size[g], HP_DECODE});
         std::sort(shapes.begin(), shapes.end());
         shapes.erase(std::unique(shapes.begin(), shapes.end()), shapes.end());
+        return shapes;
+    }
+
+    void load_kernels() {
+        const auto shapes = round_shapes();
         int64_t rows = 1;
         for (const auto& sh : shapes) rows = std::max(rows, sh.first);
         void* x = nullptr;
         cuda_ok(cudaMalloc(&x, static_cast<size_t>(rows) * h1 * 2 * 2), "cudaMalloc scratch");
-        cuda_ok(hp::launch_synth(x, rows * h1, seed_for({5}), 0.0, 1.0, cs), "synth scratch");
+        cuda_ok(hp::launch_synth(x, rows * h1, seed_for(opt.seed, {5}), 0.0, 1.0, cs), "synth scratch");
         for (const auto& sh : shapes) forward(x, sh.first, sh.second, false);
         for (int g = 0; g < static_cast<int>(dplans.size()); ++g) {
             forward(dec_x[g], group_size[g], HP_DECODE, false, g);

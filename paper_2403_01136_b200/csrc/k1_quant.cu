@@ -402,8 +402,8 @@ __global__ void dequant_kernel(const uint8_t* __restrict__ packed,
         z = SYM ? 0.0f : zero[t * 128 + r];
     }
     uint32_t v[16];
-    dequant_slice32<BITS, SYM>(base, slice, s, z, bf16x2_splat_bits(s),
-                               bf16x2_splat_bits(z), v);
+    dequant_slice32<BITS, SYM>(base, slice, s, z, scale_arg<SYM>(s),
+                               zero_arg<SYM>(s, z), v);
     const int64_t k0 = static_cast<int64_t>(g) * 128 + slice * 32;
     for (int i = 0; i < 32; ++i) {
         if (k0 + i >= k_in) break;

@@ -26,6 +26,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -469,8 +470,12 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
             for (int sl = 4 * sg.g0; sl < 4 * sg.g1; sl += SPS, ++it) {
                 const int s = it % BR;
                 PROD_WAIT(&empty_b[s], ((it / BR) & 1) ^ 1);
+#ifdef HP_EXP_NOACT  // timing experiment: no activation loads (stale smem)
+                mbar_arrive_expect_tx_elect(&full_b[s], 0u);
+#else
                 mbar_arrive_expect_tx_elect(&full_b[s], static_cast<uint32_t>(C::kB));
                 tma_load_3d_elect(stage_b(s), &tmap_x, 0, mt * BN, sl >> 1, &full_b[s]);
+#endif
             }
         }
     } else if (warp == 1) {
@@ -521,9 +526,11 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
                 const uint64_t bdesc0 = umma_desc_sw128(bbase);
 #pragma unroll
                 for (int q = 0; q < SPS / 2; ++q) {  // 64-k sub-tiles (4 MMAs each)
+#ifndef HP_EXP_NOMMA  // timing experiment: no MMAs (commits only)
                     if (2 * q < nsl)
                         mma_ts_x4_elect(d_tmem, abase + q * 32, bdesc0 + q * (BN * 8), idesc,
                                         (sl > 4 * sg.g0 || q > 0) ? 1u : 0u);
+#endif
                 }
                 tc_commit_elect(&empty_b[s]);
                 tc_commit_elect(&aempty[as]);
@@ -599,8 +606,8 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
                     if (x0 + h < nsl) {
                         const int j = h >> 2;
                         uint32_t v[16];
-                        convert_slice<BITS, SYM, GS>(wv[h], sf[j], zf[j], bf16x2_splat_bits(sf[j]),
-                                                     bf16x2_splat_bits(zf[j]), v);
+                        convert_slice<BITS, SYM, GS>(wv[h], sf[j], zf[j], scale_arg<SYM>(sf[j]),
+                                                     zero_arg<SYM>(sf[j], zf[j]), v);
                         tmem_st16(tmem + lane_addr + C::A0 + as * C::ACOLS + (x0 + h) * 16, v);
                     }
                 }
@@ -838,13 +845,17 @@ cudaError_t launch_one(const CUtensorMap& map, const qgemm_args& a, int grid,
                        cudaStream_t st) {
     constexpr int SPS = kSlicesPerStage<BITS, BN>;
     using C = qgemm_cfg<BITS, BN, SPS>;
-    static bool attr_done = false;
-    if (!attr_done) {
+    // the attribute is per device: remember it per device ordinal (a racing
+    // second setter only repeats an idempotent call)
+    static std::atomic<bool> attr_done[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64 || !attr_done[dev].load(std::memory_order_acquire)) {
         cudaError_t e = cudaFuncSetAttribute(qgemm_kernel<BITS, SYM, BN, SPS>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              C::kSmem);
         if (e != cudaSuccess) return e;
-        attr_done = true;
+        if (dev >= 0 && dev < 64) attr_done[dev].store(true, std::memory_order_release);
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);

@@ -486,8 +486,8 @@ __device__ __forceinline__ void dq_stage(uint32_t slot, int r, int nsl, uint32_t
 #pragma unroll
             for (int i = 0; i < slice_words<BITS>::N; ++i) asm volatile("" : "+r"(wv[h].w[i]));
             uint32_t v[16];
-            convert_slice<BITS, SYM>(wv[h], sf[j], zf[j], bf16x2_splat_bits(sf[j]),
-                                     bf16x2_splat_bits(zf[j]), v);
+            convert_slice<BITS, SYM>(wv[h], sf[j], zf[j], scale_arg<SYM>(sf[j]),
+                                     zero_arg<SYM>(sf[j], zf[j]), v);
             tmem_st16(a_addr + h * 16, v);
         }
     }

@@ -43,6 +43,10 @@ CONFIGS = {
                             supported=[4, 8], group=1, omega="synthetic-weights"),
     "opt13b_b32_1gpu": dict(model="opt-13b", devices=1, mem=22 * GiB, B=32, supported=None,
                             group=1, omega="survey"),
+    # north_star target: OPT-30B-shaped mixed 3/4/8/16 plan on ONE B200; the
+    # 44 GiB budget (KV alone is 26.9 GB at B = 32) makes the plan mixed
+    "opt30b_b32_1gpu": dict(model="opt-30b", devices=1, mem=44 * GiB, B=32, supported=None,
+                            group=1, omega="survey"),
     "opt30b_b32_2gpu": dict(model="opt-30b", devices=2, mem=24 * GiB, B=32, supported=None,
                             group=2, omega="survey"),
     "opt30b_b32_4gpu": dict(model="opt-30b", devices=4, mem=12 * GiB, B=32, supported=None,
