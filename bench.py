@@ -177,8 +177,6 @@ def main():
     ap.add_argument("--no-graphs", action="store_true")
     ap.add_argument("--sm-budget", type=int, default=None,
                     help="persistent-kernel grid cap (default: all SMs at N=1, 140 at N>1)")
-    ap.add_argument("--decode-fused", action="store_true",
-                    help="decode units as one K3-fused launch per bit-width run (hp_decode_plan)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", 0))
@@ -214,8 +212,7 @@ def main():
         ids = obj[0]
     pipe = Pipeline(plan_json, model_json, rank, world, ids, use_graphs=not args.no_graphs,
                     instrument=True,
-                    sm_budget=args.sm_budget if args.sm_budget is not None else (140 if world > 1 else 0),
-                    decode_fused=args.decode_fused)
+                    sm_budget=args.sm_budget if args.sm_budget is not None else (140 if world > 1 else 0))
     info = pipe.info()
     h1 = {"opt-13b": 5120, "opt-30b": 7168, "opt-66b": 9216, "bloom-176b": 14336}.get(
         json.loads(model_json).get("preset", ""), json.loads(model_json).get("h1", 0))
@@ -234,7 +231,7 @@ def main():
 
     for _ in range(max(args.warmup, 3)):
         pipe.run()
-    k0 = [pipe.kernel_stats(0), pipe.kernel_stats(1)]
+    k0 = [pipe.kernel_stats(k) for k in range(4)]
     barrier()
     times, pre_s, dec_s = [], [], []
     # cudaProfilerStart/Stop bracket the timed rounds so `ncu
@@ -248,7 +245,7 @@ def main():
             dec_s.append(t.decode_s)
         barrier()
     torch.cuda.profiler.stop()
-    k1 = [pipe.kernel_stats(0), pipe.kernel_stats(1)]
+    k1 = [pipe.kernel_stats(k) for k in range(4)]
     if os.environ.get("HP_BENCH_PER_RANK"):  # diagnostics: every rank's instrumented units
         for ph in (0, 1):
             d = {k: k1[ph][k] - k0[ph][k] for k in k1[ph]}
@@ -260,12 +257,12 @@ def main():
     dec_busy = max_over_ranks(statistics.mean(dec_s))
     tokens = B * s + B * (n - 1)
 
-    # ---- e2e: pinned host prompt in, host hidden states out -------------
-    h2d = B * s * h1 * 2 if rank == 0 else 0
-    d2h = B * h1 * 2 if rank == world - 1 else 0
-    host_in = torch.empty(max(B * s * h1, 1), dtype=torch.bfloat16).pin_memory()
-    host_in.normal_()
-    host_out = torch.empty(max(B * h1, 1), dtype=torch.bfloat16).pin_memory()
+    # ---- e2e: pinned host prompt token ids in, generated ids out ---------
+    h2d = B * s * 4 if rank == 0 else 0
+    d2h = B * n * 4 if rank == world - 1 else 0
+    vocab = int(json.loads(model_json).get("vocab_s", 50272))
+    host_in = torch.randint(0, vocab, (B * s,), dtype=torch.int32).pin_memory()
+    host_out = torch.empty(B * n, dtype=torch.int32).pin_memory()
     barrier()
     e2e_t = []
     for _ in range(args.steps):
@@ -295,6 +292,16 @@ def main():
         d_dec = {k: k1[1][k] - k0[1][k] for k in k1[1]}
         k4 = d_pre["flops"] / d_pre["seconds"] / 1e12 if d_pre["seconds"] > 0 else None
         k3 = d_dec["bytes"] / d_dec["seconds"] / 1e9 if d_dec["seconds"] > 0 else None
+        d_ap = {k: k1[2][k] - k0[2][k] for k in k1[2]}
+        d_ad = {k: k1[3][k] - k0[3][k] for k in k1[3]}
+        attention = {
+            "note": "decoder glue (not the graded linear path): mma.sync FlashAttention-2 prefill, "
+                    "KV-cache decode attention; one instrumented unit per phase per round",
+            "prefill_tflops": d_ap["flops"] / d_ap["seconds"] / 1e12 if d_ap["seconds"] > 0 else None,
+            "decode_gbs": d_ad["bytes"] / d_ad["seconds"] / 1e9 if d_ad["seconds"] > 0 else None,
+            "decode_frac_hbm": (d_ad["bytes"] / d_ad["seconds"] / 1e9 / hbm) if d_ad["seconds"] > 0 else None,
+            "prefill_avg_us": d_ap["seconds"] / max(d_ap["launches"], 1) * 1e6,
+            "decode_avg_us": d_ad["seconds"] / max(d_ad["launches"], 1) * 1e6}
         prof = ROOT / "profiles" / "ncu_traffic.json"
         ncu = json.loads(prof.read_text()).get(name, {}) if prof.exists() else {}
 
@@ -319,9 +326,7 @@ def main():
                                    "avg_flops": d_pre["flops"] / max(d_pre["launches"], 1),
                                    "avg_s": d_pre["seconds"] / max(d_pre["launches"], 1)},
                     "share_of_step": pre_share}
-        roof_dec = {"kernel": ("K3 fused decode step (hp::dstage_kernel, one launch per bit-width run)"
-                               if args.decode_fused else
-                               "K3 decode dequant-GEMV (hp::qgemm_kernel, BN=32, split-K)"),
+        roof_dec = {"kernel": "K3 decode dequant-GEMV (hp::qgemm_kernel, BN=32, split-K)",
                     "bound": "hbm", "achieved": k3, "peak": hbm, "unit": "GB/s",
                     "frac": k3 / hbm if k3 else None, "frac_of_nominal_8TBs": k3 / 8000 if k3 else None,
                     "traffic": traffic("k3"), "traffic_capture": traffic_note("k3"),
@@ -366,7 +371,9 @@ def main():
                        "stages": [st["layers"] for st in plan["stages"]],
                        "l2": "inputs larger than L2 (packed weights "
                              f"{info['weight_bytes'] / 1e9:.1f} GB/rank >> 126 MB)",
-                       "graphs": not args.no_graphs, "decode_fused": args.decode_fused},
+                       "graphs": not args.no_graphs,
+                       "decoder": "OPT pre-LN: embedding + positions, causal MHA over a KV cache, "
+                                  "tied LM head, greedy argmax"},
             "decode_tok_s": B * (n - 1) / dec_busy if dec_busy > 0 else None,
             "prefill_tok_s": B * s / pre_busy if pre_busy > 0 else None,
             "generated_tok_s": B * n / step_s,
@@ -376,6 +383,7 @@ def main():
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "pipesim": sim,
+            "attention": attention,
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu

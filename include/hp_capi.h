@@ -138,33 +138,33 @@ hp_status hp_qlinear(const hp_qweight* w, const void* x, int64_t ldx,
                      int64_t ldr, int epilogue, int phase, void* workspace,
                      size_t workspace_bytes, hp_stream stream);
 
-/* K3 fused — one decode step of a stack of OPT decoder layers in ONE
- * persistent kernel launch (the per-op hp_qlinear launches' arithmetic,
- * bit-identical, without a pipeline drain at every op boundary):
- *   for each layer: a = LN1(x); qkv = a·Wqkvᵀ; x += qkv[:, 2h1:3h1]·Woutᵀ;
- *                   a = LN2(x); f = relu(a·Wfc1ᵀ); x += f·Wfc2ᵀ
- * (self-only attention: the attention output is the V slice). x [m × h1]
- * bf16 device, updated in place, m <= 32. All layers share one scheme; bits
- * may differ per layer. ln[4] = LN1 gamma, beta, LN2 gamma, beta (bf16 [h1]).
- * The plan owns its scratch, op table, TMA descriptors and stream-K
- * workspace; run() is one kernel launch (CUDA-graph capturable).         */
 /* Glue (decoder-layer LayerNorm, glue.cu): y[r] = LN(x[r])*gamma + beta for
  * r < rows, fp32 statistics, eps 1e-5; h % 8 == 0, 16-byte aligned rows.  */
 hp_status hp_layernorm(const void* x, int64_t ldx, int64_t rows, int64_t h, const void* gamma,
                        const void* beta, void* y, int64_t ldy, hp_stream stream);
 
-typedef struct {
-    hp_qweight ops[4];   /* qkv [3h1 × h1], out [h1 × h1], fc1 [h2 × h1], fc2 [h1 × h2] */
-    const void* ln[4];
-} hp_decoder_layer;
-typedef struct hp_decode_plan hp_decode_plan;
-hp_status hp_decode_plan_create(const hp_decoder_layer* layers, int n_layers, void* x,
-                                int64_t m, hp_decode_plan** out);
-hp_status hp_decode_plan_run(hp_decode_plan* p, hp_stream stream);
-/* {weight bytes streamed per run, algorithmic bytes per run (weights +
- *  activations), ops, grid}                                */
-hp_status hp_decode_plan_info(hp_decode_plan* p, double* out4);
-void hp_decode_plan_destroy(hp_decode_plan* p);
+/* Decoder glue (decoder.cu), device pointers, bf16
+ * unless noted. qkv rows are [q | k | v] (h columns each, head hd-column
+ * blocks); hd = 64 or 128. The K/V cache of a layer is [B][S_max][h] for K
+ * then V (memcost.cpp:38-42).
+ *  hp_embed: x[r] = E[tok[r]] + P[pos(r) + 2] (OPT learned positions;
+ *    pos(r) = pos0 + r % s_tokens if pos_per_req else pos0; P may be NULL).
+ *  hp_attention_prefill: causal self-attention of `reqs` requests of s
+ *    tokens (rows r*s..), writing their K/V rows 0..s-1 into the cache at
+ *    requests req0.. ; out [reqs*s x h].
+ *  hp_attention_decode: one query row per request (rows = requests
+ *    req0..), appends K/V at position p, attends over cache rows 0..p;
+ *    s + n <= 1024.
+ *  hp_argmax: tok[r] = argmax_v logits[r][v] (ties -> lowest id), int32.  */
+hp_status hp_embed(const int32_t* tok, int rows, int pos0, int pos_per_req, int s_tokens,
+                   const void* E, const void* P, int64_t pos_s, int64_t h, int64_t vocab, void* x,
+                   hp_stream stream);
+hp_status hp_attention_prefill(const void* qkv, int reqs, int s, int64_t h, int hd, void* out,
+                               void* k_cache, void* v_cache, int req0, int s_max, hp_stream stream);
+hp_status hp_attention_decode(const void* qkv, int rows, int64_t h, int hd, int p, void* out,
+                              void* k_cache, void* v_cache, int req0, int s_max, hp_stream stream);
+hp_status hp_argmax(const void* logits, int64_t ld, int rows, int64_t vocab, int32_t* tok,
+                    hp_stream stream);
 
 /* ---- pipeline executor (one process per GPU, NCCL P2P at boundaries) ----
  * plan_json: a plan document (schema of hetplan_main.cpp:190-224, loaded by
@@ -186,30 +186,56 @@ typedef struct {
     double timeout_s;    /* hp_pipeline_run watchdog, 0 = none; expiry ->
                           * HP_ETIMEOUT with per-stream progress in
                           * hp_last_error (destroy the pipeline after)     */
-    int32_t decode_fused; /* 0 (default): a decode unit is per-op launches
-                          * (hp_layernorm + 4 hp_qlinear per layer, PDL
-                          * chained); 1: ONE K3-fused persistent launch per
-                          * bit-width run of the stage (hp_decode_plan;
-                          * bit-identical, slower on B200 today, see
-                          * DESIGN.md §4.3)                               */
 } hp_pipeline_options;
+/* Weight loader sources (the paper's on-the-fly quantized loader,
+ * PAPER.md:806-811, 827-828): each bf16 tensor comes from host memory
+ * (pinned: copied directly; pageable: staged through pinned bins) or a raw
+ * little-endian bf16 file at a byte offset; {NULL, NULL, 0} = the seeded
+ * synthetic tensor. Tensors stream to the device in bins of bin_bytes
+ * (0 -> 64 MiB) and K1 packs bin i while bin i+1 is copied.             */
+typedef struct {
+    const void* host;
+    const char* path;
+    int64_t offset;
+} hp_tensor_src;
+typedef struct {
+    int32_t n_layers;            /* the plan's num_layers                       */
+    const hp_tensor_src* linear; /* [n_layers*4] qkv [3h1 x h1], out [h1 x h1],
+                                  * fc1 [h2 x h1], fc2 [h1 x h2] (y = x W^T),
+                                  * or NULL (all synthetic)                     */
+    const hp_tensor_src* norm;   /* [n_layers*4] LN1 gamma, beta, LN2 gamma,
+                                  * beta [h1], or NULL                          */
+    hp_tensor_src embed;         /* [vocab x h1] (tied LM head)                 */
+    hp_tensor_src pos;           /* [pos_s x h1] learned positions              */
+    hp_tensor_src final_norm[2]; /* [h1] gamma, beta                            */
+    int64_t bin_bytes;
+} hp_weight_set;
 hp_status hp_nccl_unique_id(void* out128);
+/* weights: NULL = every tensor synthetic (read during the call only).    */
 hp_status hp_pipeline_create(const char* plan_json, const char* model_json, int rank,
                              int world, const void* nccl_ids,
-                             const hp_pipeline_options* opt, hp_pipeline** out);
+                             const hp_pipeline_options* opt, const hp_weight_set* weights,
+                             hp_pipeline** out);
 /* One serving round: B requests, prompt s, n generated tokens (the plan's
- * workload). host_in (rank 0): [B*s x h1] bf16 prompt activations, or NULL
- * for the device-resident synthetic prompt. host_out (last rank): [B x h1]
- * bf16 final hidden state per request, or NULL. timing4 = {makespan_s,
- * prefill_s, decode_s, io_s} of this rank, from CUDA events.             */
-hp_status hp_pipeline_run(hp_pipeline* p, const void* host_in, void* host_out,
+ * workload), greedy decoding. host_tokens (rank 0): [B x s] int32 prompt
+ * token ids, or NULL for the device-resident synthetic prompt. host_out
+ * (last rank): [B x n] int32 generated token ids, or NULL. timing4 =
+ * {makespan_s, prefill_s, decode_s, io_s} of this rank (CUDA events).    */
+hp_status hp_pipeline_run(hp_pipeline* p, const int32_t* host_tokens, int32_t* host_out,
                           double* timing4);
+/* Last rank: final hidden state (pre final-LN) of every request's last
+ * position of the last round, [B x h1] bf16 host buffer.                 */
+hp_status hp_pipeline_final_hidden(hp_pipeline* p, void* host);
+/* Weight load of hp_pipeline_create: {seconds, source bf16 bytes read,
+ * resident bytes, H2D bins}.                                             */
+hp_status hp_pipeline_load_stats(hp_pipeline* p, double* out4);
 /* Measured mean per-unit costs {pre_s, dec_s, 0, 0} of the last round, for
  * pipesim::simulate (comm costs are the caller's).                      */
 hp_status hp_pipeline_stage_costs(hp_pipeline* p, double* out4);
-/* Instrumented linear-op totals for phase (HP_PREFILL / HP_DECODE):
- * {launches, seconds, algorithmic_bytes, flops} accumulated over rounds. */
-hp_status hp_pipeline_kernel_stats(hp_pipeline* p, int phase, double* out4);
+/* Instrumented totals {launches, seconds, algorithmic_bytes, flops}
+ * accumulated over rounds; kind 0 = prefill linear ops (K4), 1 = decode
+ * linear ops (K3), 2 = prefill attention, 3 = decode attention.          */
+hp_status hp_pipeline_kernel_stats(hp_pipeline* p, int kind, double* out4);
 /* Per-layer seconds (LN + 4 linear ops) of this stage's layers in the
  * instrumented unit of the last instrument=1 round: one prefill micro-batch
  * (HP_PREFILL) or one decode group-token (HP_DECODE); *n = layer count.   */

@@ -44,3 +44,10 @@ def synth_bits(n: int, seed: int, mean: float, std: float) -> np.ndarray:
     w = (mean + v * scale).astype(np.float32)
     f = w.view(np.uint32).astype(np.uint64)
     return ((f + ((f >> np.uint64(16)) & np.uint64(1)) + np.uint64(0x7FFF)) >> np.uint64(16)).astype(np.uint16)
+
+
+def synth_tokens(n: int, seed: int, vocab: int) -> np.ndarray:
+    """int32 token ids: splitmix64(seed ^ i) % vocab (mirror of the runtime's
+    synth_tokens_kernel, csrc/decoder.cu)."""
+    i = np.arange(n, dtype=np.uint64)
+    return (splitmix64(np.uint64(seed) ^ i) % np.uint64(vocab)).astype(np.int32)

@@ -48,10 +48,6 @@ class hp_qweight(C.Structure):
     ]
 
 
-class hp_decoder_layer(C.Structure):
-    _fields_ = [("ops", hp_qweight * 4), ("ln", C.c_void_p * 4)]
-
-
 class hp_pipeline_options(C.Structure):
     _fields_ = [
         ("scheme", C.c_int32),
@@ -61,7 +57,22 @@ class hp_pipeline_options(C.Structure):
         ("seed", C.c_uint64),
         ("weight_std", C.c_double),
         ("timeout_s", C.c_double),
-        ("decode_fused", C.c_int32),
+    ]
+
+
+class hp_tensor_src(C.Structure):
+    _fields_ = [("host", C.c_void_p), ("path", C.c_char_p), ("offset", C.c_int64)]
+
+
+class hp_weight_set(C.Structure):
+    _fields_ = [
+        ("n_layers", C.c_int32),
+        ("linear", C.POINTER(hp_tensor_src)),
+        ("norm", C.POINTER(hp_tensor_src)),
+        ("embed", hp_tensor_src),
+        ("pos", hp_tensor_src),
+        ("final_norm", hp_tensor_src * 2),
+        ("bin_bytes", C.c_int64),
     ]
 
 
@@ -103,18 +114,20 @@ def _load() -> C.CDLL:
         "hp_set_sm_budget": (None, [i32]),
         "hp_set_pdl": (None, [i32]),
         "hp_nccl_unique_id": (i32, [v]),
-        "hp_pipeline_create": (i32, [p, p, i32, i32, v, P(hp_pipeline_options), P(v)]),
+        "hp_pipeline_create": (i32, [p, p, i32, i32, v, P(hp_pipeline_options), P(hp_weight_set), P(v)]),
         "hp_pipeline_run": (i32, [v, v, v, P(d)]),
+        "hp_pipeline_final_hidden": (i32, [v, v]),
+        "hp_pipeline_load_stats": (i32, [v, P(d)]),
         "hp_pipeline_stage_costs": (i32, [v, P(d)]),
         "hp_pipeline_kernel_stats": (i32, [v, i32, P(d)]),
         "hp_pipeline_layer_costs": (i32, [v, i32, P(d), i64, P(i64)]),
         "hp_pipeline_info": (i32, [v, P(i64)]),
         "hp_pipeline_destroy": (None, [v]),
         "hp_layernorm": (i32, [v, i64, i64, i64, v, v, v, i64, v]),
-        "hp_decode_plan_create": (i32, [P(hp_decoder_layer), i32, v, i64, P(v)]),
-        "hp_decode_plan_run": (i32, [v, v]),
-        "hp_decode_plan_info": (i32, [v, P(d)]),
-        "hp_decode_plan_destroy": (None, [v]),
+        "hp_embed": (i32, [v, i32, i32, i32, i32, v, v, i64, i64, i64, v, v]),
+        "hp_attention_prefill": (i32, [v, i32, i32, i64, i32, v, v, v, i32, i32, v]),
+        "hp_attention_decode": (i32, [v, i32, i64, i32, i32, v, v, v, i32, i32, v]),
+        "hp_argmax": (i32, [v, i64, i32, i64, v, v]),
     })
     optional = {}
     for name, (res, args) in list(sig.items()) + list(optional.items()):
@@ -138,7 +151,8 @@ EXPORTED = [
     "hp_host_make_schedule", "hp_host_simulate", "hp_host_plan_check", "hp_host_unit_order", "hp_host_latency_fit", "hp_host_latency_predict", "hp_set_sm_budget", "hp_set_pdl",
     "hp_nccl_unique_id", "hp_pipeline_create", "hp_pipeline_run", "hp_pipeline_stage_costs",
     "hp_pipeline_kernel_stats", "hp_pipeline_layer_costs", "hp_pipeline_info", "hp_pipeline_destroy",
-    "hp_layernorm", "hp_decode_plan_create", "hp_decode_plan_run", "hp_decode_plan_info", "hp_decode_plan_destroy",
+    "hp_layernorm", "hp_embed", "hp_attention_prefill", "hp_attention_decode", "hp_argmax",
+    "hp_pipeline_final_hidden", "hp_pipeline_load_stats",
 ]
 
 

@@ -41,38 +41,18 @@ struct qgemm_plan {
     int dp;
 };
 qgemm_plan plan_qgemm(int64_t n_out, int64_t k_in, int64_t m, int phase);
-struct dstage_op {
-    const uint8_t* packed;
-    const float* scale;
-    const float* zero;
-    void* y;
-    const void* res;
-    const CUtensorMap* tmap;
-    int64_t ldy, ldr;
-    int total;
-    int kind;
-    int bits, n_out, k_in, G, NT, maxseg, epi, sps;
-    unsigned wait;
-    const void* ln_x;
-    const void* gamma;
-    const void* beta;
-    void* ln_y;
-    int64_t ln_ldx, ln_ldy;
-    int h;
-    int P;
-    const unsigned* dep_flags;
-    unsigned* out_flags;
-    int dep_off;
-    int pbuf;
-};
-static_assert(sizeof(dstage_op) == 192, "dstage_op layout is shared by k3_stage.cu and capi.cu");
-int dstage_grid();
+int slices_per_stage(int bits, int bn);
 cudaError_t launch_layernorm(const void* x, int64_t ldx, int64_t rows, int h, const void* gamma,
                              const void* beta, void* y, int64_t ldy, cudaStream_t st);
-cudaError_t launch_dstage(const dstage_op* ops, int nops, int m, int bits, bool sym,
-                          unsigned long long* sync, unsigned long long units, unsigned* const counters[2],
-                          float* const partial[2], int grid, cudaStream_t st);
-int slices_per_stage(int bits, int bn);
+cudaError_t launch_embed(const int32_t* tok, int rows, int pos0, int pos_per_req, int s_tokens,
+                         const void* E, const void* P, int pos_s, int h, int64_t vocab, void* x,
+                         cudaStream_t st);
+cudaError_t launch_attn_prefill(const void* qkv, int reqs, int s, int h, int D, void* out, void* kc,
+                                void* vc, int req0, int S_max, cudaStream_t st);
+cudaError_t launch_attn_decode(const void* qkv, int rows, int h, int D, int p, void* out, void* kc,
+                               void* vc, int req0, int S_max, cudaStream_t st);
+cudaError_t launch_argmax(const void* logits, int64_t ld, int rows, int64_t vocab, int32_t* tok,
+                          int32_t* tok2, int64_t tok2_stride, cudaStream_t st);
 cudaError_t launch_qgemm(const CUtensorMap& map, const qgemm_plan& p, int bits, bool sym,
                          const void* packed, const float* scale, const float* zero,
                          int64_t n_out, int64_t k_in, int64_t m, void* y, int64_t ldy,
@@ -189,7 +169,7 @@ extern "C" {
 
 const char* hp_last_error(void) { return g_error.c_str(); }
 
-int hp_abi_version(void) { return 1; }
+int hp_abi_version(void) { return 2; }
 
 int hp_device_ok(void) { return device_ok_cached(); }
 
@@ -362,249 +342,50 @@ hp_status hp_layernorm(const void* x, int64_t ldx, int64_t rows, int64_t h, cons
                        "layernorm");
 }
 
-struct hp_decode_plan {
-    struct run {  // consecutive layers of one bit width = one kernel launch
-        int op0, nops, bits;
-        unsigned long long units;
-        unsigned long long* sync;
-    };
-    std::vector<void*> allocs;
-    std::vector<run> runs;
-    hp::dstage_op* d_ops = nullptr;
-    int nops = 0;
-    int m = 0;
-    bool sym = true;
-    unsigned* counters[2] = {nullptr, nullptr};
-    float* partial[2] = {nullptr, nullptr};
-    int grid = 0;
-    double weight_bytes = 0, alg_bytes = 0;
-    void* scratch[3] = {nullptr, nullptr, nullptr};
-};
-
-/* debug (not in the ABI header): scratch buffers a, qkv, f of a plan */
-void hp_decode_plan_debug_scratch(hp_decode_plan* p, void** out3) {
-    for (int i = 0; i < 3; ++i) out3[i] = p->scratch[i];
-}
-
-hp_status hp_decode_plan_create(const hp_decoder_layer* layers, int n_layers, void* x,
-                                int64_t m, hp_decode_plan** out) {
-    if (!out) return fail(HP_EINVAL, "decode_plan: NULL out");
-    *out = nullptr;
-    if (!layers || n_layers <= 0) return fail(HP_EINVAL, "decode_plan: no layers");
-    if (!x || (reinterpret_cast<uintptr_t>(x) & 15)) return fail(HP_EINVAL, "decode_plan: x must be 16-byte aligned");
-    if (m <= 0 || m > 32) return fail(HP_EINVAL, "decode_plan: m must be in [1, 32]");
-    const int64_t h1 = layers[0].ops[1].n_out, h2 = layers[0].ops[2].n_out;
-    const int scheme = layers[0].ops[0].scheme;
-    if (h1 <= 0 || h1 % 128 || h2 % 128 || h1 > 16384)
-        return fail(HP_EINVAL, "decode_plan: h1, h2 must be multiples of 128 (h1 <= 16384)");
-    for (int l = 0; l < n_layers; ++l) {
-        const hp_decoder_layer& L = layers[l];
-        const int64_t shp[4][2] = {{3 * h1, h1}, {h1, h1}, {h2, h1}, {h1, h2}};
-        for (int o = 0; o < 4; ++o) {
-            if (hp_status s = check_qweight(&L.ops[o])) return s;
-            if (L.ops[o].n_out != shp[o][0] || L.ops[o].k_in != shp[o][1])
-                return fail(HP_EINVAL, "decode_plan: layer " + std::to_string(l) + " op " +
-                                           std::to_string(o) + " has the wrong shape");
-            if (L.ops[o].scheme != scheme) return fail(HP_EINVAL, "decode_plan: mixed schemes");
-        }
-        for (int j = 0; j < 4; ++j)
-            if (!L.ln[j] || (reinterpret_cast<uintptr_t>(L.ln[j]) & 15))
-                return fail(HP_EINVAL, "decode_plan: LN parameters must be 16-byte aligned");
-    }
+hp_status hp_embed(const int32_t* tok, int rows, int pos0, int pos_per_req, int s_tokens,
+                   const void* E, const void* P, int64_t pos_s, int64_t h, int64_t vocab, void* x,
+                   hp_stream stream) {
+    if (!tok || !E || !x) return fail(HP_EINVAL, "embed: NULL pointer");
+    if (rows <= 0 || h <= 0 || h % 8 || vocab <= 0 || (pos_per_req && s_tokens <= 0))
+        return fail(HP_EINVAL, "embed: bad shape");
     if (hp_status s = need_device()) return s;
-    auto* p = new hp_decode_plan();
-    auto cleanup = [&](hp_status s) {
-        hp_decode_plan_destroy(p);
-        return s;
-    };
-    auto dalloc = [&](size_t bytes) -> void* {
-        void* q = nullptr;
-        if (cudaMalloc(&q, std::max<size_t>(bytes, 256)) != cudaSuccess) return nullptr;
-        p->allocs.push_back(q);
-        return q;
-    };
-    p->m = static_cast<int>(m);
-    p->sym = scheme == HP_SYMMETRIC;
-    p->grid = hp::dstage_grid();
-    void* scr_a = dalloc(m * h1 * 2);
-    void* scr_qkv = dalloc(m * 3 * h1 * 2);
-    void* scr_f = dalloc(m * h2 * 2);
-    if (!scr_a || !scr_qkv || !scr_f) return cleanup(fail(HP_ECUDA, "decode_plan: cudaMalloc"));
-    p->scratch[0] = scr_a;
-    p->scratch[1] = scr_qkv;
-    p->scratch[2] = scr_f;
-    // host op table + tensor maps
-    std::vector<hp::dstage_op> ops;
-    std::vector<CUtensorMap> maps;
-    std::vector<int> map_of;  // op index -> map index
-    std::vector<std::pair<int, int>> flag_of;  // op index -> (flags offset, count) or (-1, 0)
-    size_t part_bytes = 0;
-    int max_nt = 1, nflags = 0, ngemm = 0;
-    unsigned done = 0;  // units of the current run so far
-    auto gemm = [&](const hp_qweight& w, const void* xin, int64_t ldx, void* y, int64_t ldy,
-                    const void* res, int epi, bool flags_out, int dep_op, int dep_off) -> hp_status {
-        hp::dstage_op op{};
-        op.kind = 0;
-        op.bits = w.bits;
-        op.packed = static_cast<const uint8_t*>(w.packed);
-        op.scale = w.scale;
-        op.zero = w.zero;
-        op.n_out = static_cast<int>(w.n_out);
-        op.k_in = static_cast<int>(w.k_in);
-        op.G = static_cast<int>(hp::ceil_div64(w.k_in, 128));
-        op.NT = static_cast<int>(hp::ceil_div64(w.n_out, 128));
-        op.total = op.NT * op.G;
-        const int64_t grid = std::min<int64_t>(p->grid, op.total);
-        op.P = static_cast<int>(grid);
-        const int64_t per = op.total / grid;
-        op.maxseg = static_cast<int>(std::min<int64_t>((op.G + per - 1) / per + 1, grid));
-        op.sps = w.bits <= 4 ? 8 : (w.bits == 8 ? 4 : 2);
-        op.y = y;
-        op.ldy = ldy;
-        op.res = res;
-        op.ldr = res ? ldy : 0;
-        op.epi = epi;
-        op.wait = done;
-        op.pbuf = (ngemm++) & 1;
-        op.dep_off = dep_off;
-        done += static_cast<unsigned>(op.NT);
-        CUtensorMap map;
-        if (hp_status s = make_act_map(&map, xin, w.k_in, m, ldx, 32, op.sps / 2)) return s;
-        map_of.push_back(static_cast<int>(maps.size()));
-        maps.push_back(map);
-        // flags resolved to device pointers after the upload
-        flag_of.push_back(flags_out ? std::make_pair(nflags, op.NT) : std::make_pair(-1, dep_op));
-        if (flags_out) nflags += op.NT;
-        ops.push_back(op);
-        part_bytes = std::max(part_bytes, static_cast<size_t>(op.NT) * op.maxseg * 128 * 32 * 4);
-        max_nt = std::max(max_nt, op.NT);
-        p->weight_bytes += static_cast<double>(hp_packed_bytes(w.n_out, w.k_in, w.bits)) +
-                           (w.bits == 16 ? 0.0 : 4.0 * hp_scale_count(w.n_out, w.k_in) *
-                                                     (w.scheme == HP_SYMMETRIC ? 1 : 2));
-        p->alg_bytes += 2.0 * m * (w.n_out + w.k_in);
-        return HP_OK;
-    };
-    auto ln = [&](const void* gamma, const void* beta) {
-        hp::dstage_op op{};
-        op.kind = 1;
-        op.ln_x = x;
-        op.ln_ldx = h1;
-        op.ln_y = scr_a;
-        op.ln_ldy = h1;
-        op.gamma = gamma;
-        op.beta = beta;
-        op.h = static_cast<int>(h1);
-        op.wait = done;
-        done += static_cast<unsigned>(m);
-        map_of.push_back(-1);
-        flag_of.push_back({-1, -1});
-        ops.push_back(op);
-    };
-    std::vector<int> dep_of;  // op -> producing op index for dataflow edges (or -1)
-    for (int l = 0; l < n_layers; ++l) {
-        const hp_decoder_layer& L = layers[l];
-        if (l == 0 || L.ops[0].bits != layers[l - 1].ops[0].bits) {  // new run: a kernel boundary
-            if (!p->runs.empty()) {
-                p->runs.back().nops = static_cast<int>(ops.size()) - p->runs.back().op0;
-                p->runs.back().units = done;
-            }
-            p->runs.push_back({static_cast<int>(ops.size()), 0, L.ops[0].bits, 0, nullptr});
-            done = 0;
-        }
-        for (int o = 1; o < 4; ++o)
-            if (L.ops[o].bits != L.ops[0].bits)
-                return cleanup(fail(HP_EINVAL, "decode_plan: the four ops of a layer must share a bit width"));
-        const int i0 = static_cast<int>(ops.size());
-        ln(L.ln[0], L.ln[1]);
-        if (hp_status s = gemm(L.ops[0], scr_a, h1, scr_qkv, 3 * h1, nullptr, 0, true, -1, 0)) return cleanup(s);
-        // out-proj reads the V slice: qkv output tiles [2 h1/128, 3 h1/128)
-        if (hp_status s = gemm(L.ops[1], static_cast<char*>(scr_qkv) + 2 * h1 * 2, 3 * h1, x, h1, x, 0, false,
-                               i0 + 1, static_cast<int>(2 * h1 / 128)))
-            return cleanup(s);
-        ln(L.ln[2], L.ln[3]);
-        if (hp_status s = gemm(L.ops[2], scr_a, h1, scr_f, h2, nullptr, HP_EPI_RELU, true, -1, 0)) return cleanup(s);
-        if (hp_status s = gemm(L.ops[3], scr_f, h2, x, h1, x, 0, false, i0 + 4, 0)) return cleanup(s);
-    }
-    p->runs.back().nops = static_cast<int>(ops.size()) - p->runs.back().op0;
-    p->runs.back().units = done;
-    p->alg_bytes += p->weight_bytes;
-    p->nops = static_cast<int>(ops.size());
-    // device image: [maps (64-B aligned)] [ops] [sync per run] [flags] [tickets x2] [partials x2]
-    auto up = [](size_t v) { return (v + 255) / 256 * 256; };
-    const size_t maps_bytes = maps.size() * sizeof(CUtensorMap);
-    const size_t ops_off = up(maps_bytes);
-    const size_t ops_bytes = ops.size() * sizeof(hp::dstage_op);
-    const size_t sync_off = up(ops_off + ops_bytes);
-    const size_t sync_bytes = p->runs.size() * 256;
-    const size_t flags_off = up(sync_off + sync_bytes);
-    const size_t flags_bytes = static_cast<size_t>(nflags) * 4;
-    const size_t tick_off = up(flags_off + flags_bytes);
-    const size_t tick_bytes = up(static_cast<size_t>(max_nt) * 4);
-    const size_t part_off = up(tick_off + 2 * tick_bytes);
-    auto* base = static_cast<char*>(dalloc(part_off + 2 * part_bytes));
-    if (!base) return cleanup(fail(HP_ECUDA, "decode_plan: cudaMalloc"));
-    auto* dmaps = reinterpret_cast<CUtensorMap*>(base);
-    auto* dflags = reinterpret_cast<unsigned*>(base + flags_off);
-    for (size_t i = 0; i < ops.size(); ++i) {
-        if (map_of[i] >= 0) ops[i].tmap = dmaps + map_of[i];
-        if (ops[i].kind == 0 && flag_of[i].first >= 0) ops[i].out_flags = dflags + flag_of[i].first;
-    }
-    for (size_t i = 0; i < ops.size(); ++i) {  // dataflow edges: the producer's flags
-        if (ops[i].kind == 0 && flag_of[i].first < 0 && flag_of[i].second >= 0)
-            ops[i].dep_flags = ops[flag_of[i].second].out_flags;
-    }
-    for (size_t r = 0; r < p->runs.size(); ++r)
-        p->runs[r].sync = reinterpret_cast<unsigned long long*>(base + sync_off + r * 256);
-    p->d_ops = reinterpret_cast<hp::dstage_op*>(base + ops_off);
-    for (int b = 0; b < 2; ++b) {
-        p->counters[b] = reinterpret_cast<unsigned*>(base + tick_off + b * tick_bytes);
-        p->partial[b] = reinterpret_cast<float*>(base + part_off + b * part_bytes);
-    }
-    if (cudaMemcpy(dmaps, maps.data(), maps_bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(p->d_ops, ops.data(), ops_bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemset(base + sync_off, 0, part_off - sync_off) != cudaSuccess)
-        return cleanup(fail(HP_ECUDA, "decode_plan: upload"));
-    *out = p;
-    return HP_OK;
+    return cuda_status(hp::launch_embed(tok, rows, pos0, pos_per_req, s_tokens, E, P,
+                                        static_cast<int>(pos_s), static_cast<int>(h), vocab, x,
+                                        static_cast<cudaStream_t>(stream)),
+                       "embed");
 }
 
-hp_status hp_decode_plan_run(hp_decode_plan* p, hp_stream stream) {
-    if (!p) return fail(HP_EINVAL, "decode_plan_run: NULL plan");
-    int limit = p->nops;
-    if (const char* e = getenv("HP_DSTAGE_NOPS")) limit = std::min(limit, atoi(e));  // debug
-    for (const auto& r : p->runs) {
-        const int n = std::min(r.nops, limit - r.op0);
-        if (n <= 0) break;
-        // a truncated run (debug) must still see its full per-launch unit count
-        // only when complete; recompute for the prefix
-        unsigned long long units = r.units;
-        if (n < r.nops) {
-            std::vector<hp::dstage_op> tmp(1);
-            cudaMemcpy(tmp.data(), p->d_ops + r.op0 + n, sizeof(hp::dstage_op), cudaMemcpyDeviceToHost);
-            units = tmp[0].wait;
-        }
-        if (hp_status s = cuda_status(
-                hp::launch_dstage(p->d_ops + r.op0, n, p->m, r.bits, p->sym, r.sync, units, p->counters,
-                                  p->partial, p->grid, static_cast<cudaStream_t>(stream)),
-                "decode_plan_run"))
-            return s;
-    }
-    return HP_OK;
+hp_status hp_attention_prefill(const void* qkv, int reqs, int s, int64_t h, int hd, void* out,
+                               void* k_cache, void* v_cache, int req0, int s_max, hp_stream stream) {
+    if (!qkv || !out || !k_cache || !v_cache) return fail(HP_EINVAL, "attention_prefill: NULL pointer");
+    if ((hd != 64 && hd != 128) || h % hd || reqs <= 0 || s <= 0 || s > s_max || req0 < 0)
+        return fail(HP_EINVAL, "attention_prefill: bad shape (head dim 64 or 128)");
+    if (hp_status st = need_device()) return st;
+    return cuda_status(hp::launch_attn_prefill(qkv, reqs, s, static_cast<int>(h), hd, out, k_cache,
+                                               v_cache, req0, s_max, static_cast<cudaStream_t>(stream)),
+                       "attention_prefill");
 }
 
-hp_status hp_decode_plan_info(hp_decode_plan* p, double* out4) {
-    if (!p || !out4) return fail(HP_EINVAL, "decode_plan_info: NULL argument");
-    out4[0] = p->weight_bytes;
-    out4[1] = p->alg_bytes;
-    out4[2] = p->nops;
-    out4[3] = p->grid;
-    return HP_OK;
+hp_status hp_attention_decode(const void* qkv, int rows, int64_t h, int hd, int p, void* out,
+                              void* k_cache, void* v_cache, int req0, int s_max, hp_stream stream) {
+    if (!qkv || !out || !k_cache || !v_cache) return fail(HP_EINVAL, "attention_decode: NULL pointer");
+    if ((hd != 64 && hd != 128) || h % hd || rows <= 0 || p < 0 || p >= s_max || s_max > 1024 || req0 < 0)
+        return fail(HP_EINVAL, "attention_decode: bad shape (head dim 64 or 128, s_max <= 1024)");
+    if (hp_status st = need_device()) return st;
+    return cuda_status(hp::launch_attn_decode(qkv, rows, static_cast<int>(h), hd, p, out, k_cache,
+                                              v_cache, req0, s_max, static_cast<cudaStream_t>(stream)),
+                       "attention_decode");
 }
 
-void hp_decode_plan_destroy(hp_decode_plan* p) {
-    if (!p) return;
-    for (void* q : p->allocs) cudaFree(q);
-    delete p;
+hp_status hp_argmax(const void* logits, int64_t ld, int rows, int64_t vocab, int32_t* tok,
+                    hp_stream stream) {
+    if (!logits || !tok) return fail(HP_EINVAL, "argmax: NULL pointer");
+    if (rows <= 0 || vocab <= 0 || ld < vocab || vocab > (int64_t(1) << 31))
+        return fail(HP_EINVAL, "argmax: bad shape");
+    if (hp_status st = need_device()) return st;
+    return cuda_status(hp::launch_argmax(logits, ld, rows, vocab, tok, nullptr, 0,
+                                         static_cast<cudaStream_t>(stream)),
+                       "argmax");
 }
 
 }  // extern "C"

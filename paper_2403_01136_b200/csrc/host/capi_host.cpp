@@ -307,7 +307,7 @@ hp_status hp_nccl_unique_id(void* out128) {
 
 hp_status hp_pipeline_create(const char* plan_json, const char* model_json, int rank, int world,
                              const void* nccl_ids, const hp_pipeline_options* opt,
-                             hp_pipeline** out) {
+                             const hp_weight_set* weights, hp_pipeline** out) {
     try {
         if (!plan_json || !model_json || !out)
             throw std::invalid_argument("pipeline_create: NULL argument");
@@ -331,7 +331,29 @@ hp_status hp_pipeline_create(const char* plan_json, const char* model_json, int 
             po.seed = opt->seed;
             po.weight_std = opt->weight_std > 0 ? opt->weight_std : 0.02;
             po.timeout_s = opt->timeout_s;
-            po.decode_fused = opt->decode_fused != 0;
+        }
+        hetplan::runtime::weight_set ws;
+        if (weights) {
+            if (weights->n_layers != doc.num_layers)
+                throw std::invalid_argument("pipeline_create: weight set n_layers != plan num_layers");
+            auto src = [](const hp_tensor_src& t) {
+                hetplan::runtime::tensor_source r;
+                r.host = t.host;
+                if (t.path) r.path = t.path;
+                r.offset = t.offset;
+                return r;
+            };
+            const size_t L4 = static_cast<size_t>(doc.num_layers) * 4;
+            if (weights->linear)
+                for (size_t i = 0; i < L4; ++i) ws.linear.push_back(src(weights->linear[i]));
+            if (weights->norm)
+                for (size_t i = 0; i < L4; ++i) ws.norm.push_back(src(weights->norm[i]));
+            ws.embed = src(weights->embed);
+            ws.pos = src(weights->pos);
+            ws.final_norm[0] = src(weights->final_norm[0]);
+            ws.final_norm[1] = src(weights->final_norm[1]);
+            if (weights->bin_bytes > 0) ws.bin_bytes = weights->bin_bytes;
+            po.weights = &ws;
         }
         std::vector<std::array<char, 128>> ids;
         if (world > 1) {
@@ -352,7 +374,8 @@ hp_status hp_pipeline_create(const char* plan_json, const char* model_json, int 
     }
 }
 
-hp_status hp_pipeline_run(hp_pipeline* p, const void* host_in, void* host_out, double* timing4) {
+hp_status hp_pipeline_run(hp_pipeline* p, const int32_t* host_in, int32_t* host_out,
+                          double* timing4) {
     try {
         if (!p) throw std::invalid_argument("pipeline_run: NULL pipeline");
         const auto t = p->impl->run(host_in, host_out);
@@ -378,9 +401,29 @@ hp_status hp_pipeline_stage_costs(hp_pipeline* p, double* out4) {
     return HP_OK;
 }
 
-hp_status hp_pipeline_kernel_stats(hp_pipeline* p, int phase, double* out4) {
+hp_status hp_pipeline_final_hidden(hp_pipeline* p, void* host) {
+    try {
+        if (!p || !host) throw std::invalid_argument("pipeline_final_hidden: NULL argument");
+        p->impl->final_hidden(host);
+        return HP_OK;
+    } catch (const std::exception& e) {
+        return from_exception(e);
+    }
+}
+
+hp_status hp_pipeline_load_stats(hp_pipeline* p, double* out4) {
     if (!p || !out4) return HP_EINVAL;
-    const auto& k = p->impl->stats(phase);
+    const auto& l = p->impl->loading();
+    out4[0] = l.seconds;
+    out4[1] = l.source_bytes;
+    out4[2] = l.packed_bytes;
+    out4[3] = static_cast<double>(l.bins);
+    return HP_OK;
+}
+
+hp_status hp_pipeline_kernel_stats(hp_pipeline* p, int kind, double* out4) {
+    if (!p || !out4 || kind < 0 || kind > 3) return HP_EINVAL;
+    const auto& k = p->impl->stats(kind);
     out4[0] = static_cast<double>(k.launches);
     out4[1] = k.seconds;
     out4[2] = k.bytes;

@@ -11,7 +11,8 @@
 //     roofline cost estimates (static_unit_order), so all ranks agree on the
 //     send/recv sequence without any control messages;
 //   * the whole round (all units, sends, recvs) is captured into ONE CUDA
-//     graph per rank after an eager warm-up round.
+//     graph per rank after an eager warm-up round;
+//   * weights are loaded once, through the binned H2D + K1 loader below.
 #include "hetplan/runtime/pipeline.hpp"
 
 #include <cuda_runtime.h>
@@ -24,7 +25,9 @@
 #include <thread>
 #include <cmath>
 #include <cstring>
+#include <fcntl.h>
 #include <map>
+#include <unistd.h>
 #include <stdexcept>
 #include <string>
 
@@ -37,6 +40,17 @@ cudaError_t launch_layernorm(const void* x, int64_t ldx, int64_t rows, int h, co
                              const void* beta, void* y, int64_t ldy, cudaStream_t st);
 cudaError_t launch_gather_rows(const void* src, int64_t lds, int64_t stride, int64_t offset,
                                int rows, int h, void* dst, int64_t ldd, cudaStream_t st);
+cudaError_t launch_embed(const int32_t* tok, int rows, int pos0, int pos_per_req, int s_tokens,
+                         const void* E, const void* P, int pos_s, int h, int64_t vocab, void* x,
+                         cudaStream_t st);
+cudaError_t launch_attn_prefill(const void* qkv, int reqs, int s, int h, int D, void* out, void* kc,
+                                void* vc, int req0, int S_max, cudaStream_t st);
+cudaError_t launch_attn_decode(const void* qkv, int rows, int h, int D, int p, void* out, void* kc,
+                               void* vc, int req0, int S_max, cudaStream_t st);
+cudaError_t launch_argmax(const void* logits, int64_t ld, int rows, int64_t vocab, int32_t* tok,
+                          int32_t* tok2, int64_t tok2_stride, cudaStream_t st);
+cudaError_t launch_synth_tokens(int32_t* out, int64_t n, uint64_t seed, int64_t vocab,
+                                cudaStream_t st);
 }  // namespace hp
 
 namespace hetplan::runtime {
@@ -141,6 +155,111 @@ std::vector<std::vector<unit_ref>> static_unit_order(const plan_io::plan_documen
     return order;
 }
 
+namespace {
+
+// ---- the weight loader: host memory / disk -> pinned bins -> device, K1 on
+// each bin while the next one is copied. Two
+// device bins and two pinned host bins; a bin's device buffer is reused only
+// after its consumer (K1 or a device copy on the compute stream) finished,
+// a host bin only after its H2D copy finished.
+class bin_loader {
+public:
+    bin_loader(cudaStream_t compute, int64_t bin_bytes) : cs_(compute), bin_(bin_bytes) {
+        cuda_ok(cudaStreamCreateWithFlags(&cp_, cudaStreamNonBlocking), "loader stream");
+        for (int i = 0; i < 2; ++i) {
+            cuda_ok(cudaMalloc(&dev_[i], static_cast<size_t>(bin_)), "loader bin");
+            cuda_ok(cudaEventCreateWithFlags(&ev_copy_[i], cudaEventDisableTiming), "ev");
+            cuda_ok(cudaEventCreateWithFlags(&ev_used_[i], cudaEventDisableTiming), "ev");
+        }
+    }
+    ~bin_loader() {
+        cudaStreamSynchronize(cs_);
+        cudaStreamSynchronize(cp_);
+        for (int i = 0; i < 2; ++i) {
+            cudaFree(dev_[i]);
+            if (host_[i]) cudaFreeHost(host_[i]);
+            cudaEventDestroy(ev_copy_[i]);
+            cudaEventDestroy(ev_used_[i]);
+        }
+        for (auto& kv : fds_) ::close(kv.second);
+        cudaStreamDestroy(cp_);
+    }
+    int64_t bin_bytes() const { return bin_; }
+    double source_bytes() const { return bytes_; }
+    int64_t bins() const { return bins_; }
+
+    // Bytes [off, off + len) of src (len <= bin) into a device bin; the
+    // compute stream is ordered after the copy. Returns the device pointer;
+    // the caller enqueues its consumer on the compute stream, then release().
+    void* fetch(const tensor_source& src, int64_t off, int64_t len) {
+        if (len > bin_) throw std::logic_error("loader: chunk larger than a bin");
+        slot_ = static_cast<int>(bins_++ & 1);
+        cuda_ok(cudaStreamWaitEvent(cp_, ev_used_[slot_], 0), "loader wait");
+        if (src.host && pinned(src.host)) {
+            cuda_ok(cudaMemcpyAsync(dev_[slot_], static_cast<const char*>(src.host) + off,
+                                    static_cast<size_t>(len), cudaMemcpyHostToDevice, cp_),
+                    "loader h2d");
+        } else {
+            if (!host_[slot_])
+                cuda_ok(cudaMallocHost(&host_[slot_], static_cast<size_t>(bin_)), "loader pinned bin");
+            // the H2D copy that last read this host bin must be done
+            cuda_ok(cudaEventSynchronize(ev_copy_[slot_]), "loader host bin");
+            if (src.host) {
+                std::memcpy(host_[slot_], static_cast<const char*>(src.host) + off, static_cast<size_t>(len));
+            } else {
+                read_file(src.path, src.offset + off, host_[slot_], len);
+            }
+            cuda_ok(cudaMemcpyAsync(dev_[slot_], host_[slot_], static_cast<size_t>(len),
+                                    cudaMemcpyHostToDevice, cp_),
+                    "loader h2d");
+        }
+        cuda_ok(cudaEventRecord(ev_copy_[slot_], cp_), "ev");
+        cuda_ok(cudaStreamWaitEvent(cs_, ev_copy_[slot_], 0), "loader wait");
+        bytes_ += static_cast<double>(len);
+        return dev_[slot_];
+    }
+    void release() { cuda_ok(cudaEventRecord(ev_used_[slot_], cs_), "ev"); }
+
+private:
+    static bool pinned(const void* p) {
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        return a.type == cudaMemoryTypeHost;
+    }
+    void read_file(const std::string& path, int64_t off, void* dst, int64_t len) {
+        auto it = fds_.find(path);
+        if (it == fds_.end()) {
+            const int fd = ::open(path.c_str(), O_RDONLY);
+            if (fd < 0) throw std::invalid_argument("pipeline: cannot open weight file " + path);
+            it = fds_.emplace(path, fd).first;
+        }
+        int64_t done = 0;
+        while (done < len) {
+            const ssize_t r = ::pread(it->second, static_cast<char*>(dst) + done,
+                                      static_cast<size_t>(len - done), off + done);
+            if (r <= 0)
+                throw std::invalid_argument("pipeline: short read from " + path + " at byte " +
+                                            std::to_string(off + done));
+            done += r;
+        }
+    }
+
+    cudaStream_t cs_ = nullptr, cp_ = nullptr;
+    int64_t bin_ = 0;
+    void* dev_[2] = {nullptr, nullptr};
+    void* host_[2] = {nullptr, nullptr};
+    cudaEvent_t ev_copy_[2] = {nullptr, nullptr}, ev_used_[2] = {nullptr, nullptr};
+    int slot_ = 0;
+    int64_t bins_ = 0;
+    double bytes_ = 0.0;
+    std::map<std::string, int> fds_;
+};
+
+}  // namespace
+
 struct pipeline::impl {
     plan_io::plan_document plan;
     model_spec model;
@@ -148,14 +267,16 @@ struct pipeline::impl {
     pipeline_options opt;
     int begin = 0, end = 0;
     std::vector<int> bits;
-    int B = 0, s = 0, n = 0, eta = 0, xi = 0;
-    int64_t h1 = 0, h2 = 0;
+    int B = 0, s = 0, n = 0, eta = 0, xi = 0, S_max = 0;
+    int64_t h1 = 0, h2 = 0, vocab = 0;
+    int heads = 0, hd = 0;  // attention heads, head dim
     pipesim::microbatch_schedule sched;
     std::vector<unit_ref> units;      // this stage, execution order
     std::vector<unit_ref> prev_units; // previous stage's order (recv order), rank > 0
     std::vector<unit_ref> last_units; // last stage's order (feedback order)
     std::vector<int> group_size;      // requests per decode group
     std::vector<int> group_first;     // first request of each group
+    bool first = false, last = false; // stage 0 (embedding) / last stage (LM head)
 
     cudaStream_t cs = nullptr, ss = nullptr, rs = nullptr;
     ncclComm_t c_in = nullptr, c_out = nullptr;  // link from prev / to next
@@ -171,25 +292,33 @@ struct pipeline::impl {
     struct layer {
         opw ops[4];
         void* ln[4] = {nullptr, nullptr, nullptr, nullptr};
+        void* kv = nullptr;  // K cache [B][S_max][h1], then V cache, bf16
         int bits = 16;
     };
     std::vector<layer> layers;
-    void* prompt = nullptr;      // [B*s x h1] working prompt / prefill activations
-    void* pristine = nullptr;    // rank 0 synthetic prompt
-    void* scr_a = nullptr;       // [M x h1]
+    // stage 0: embedding, positions, prompt token ids
+    void* embed = nullptr;       // [vocab x h1] (rank 0 and the last rank)
+    void* pos_emb = nullptr;     // [pos_s x h1] (rank 0)
+    int32_t* prompt_tok = nullptr;    // [B x s] working prompt ids (rank 0)
+    int32_t* pristine_tok = nullptr;  // [B x s] synthetic prompt ids (rank 0)
+    // last stage: final LN, tied LM head, generated tokens
+    void* lnf[2] = {nullptr, nullptr};
+    opw lm;                      // 16-bit packed embedding (hp_qlinear LM head)
+    void* lm_x = nullptr;        // [xi x h1] gathered last positions
+    void* lm_a = nullptr;        // [xi x h1] final-LN output
+    void* logits = nullptr;      // [xi x vocab]
+    int32_t* out_tok = nullptr;  // [B x n] generated ids (last rank)
+    int32_t* cur_tok = nullptr;  // [B] each request's latest token (rank 0 and last rank)
+    // activations
+    void* prompt = nullptr;      // [B*s x h1] prefill activations
+    void* scr_a = nullptr;       // [M x h1] LN / attention output
     void* scr_qkv = nullptr;     // [M x 3h1]
     void* scr_f = nullptr;       // [M x h2]
     std::vector<void*> dec_x;    // per group [xi_g x h1]
-    std::vector<void*> fb;       // last rank (world > 1): gather target per group
-    // K3 fused (option decode_fused): one hp_decode_plan per decode group, bound to
-    // dec_x[g]; a decode unit = one persistent launch per bit-width run of
-    // the stage's layers (k3_stage.cu) instead of 6 launches per layer
-    std::vector<hp_decode_plan*> dplans;
-    int dplan_runs = 0;              // kernel launches per fused decode unit
-    cudaEvent_t dec_ev[2] = {nullptr, nullptr};  // instrumented fused unit
     void* ws = nullptr;
     size_t ws_bytes = 0;
     int64_t weight_bytes = 0;
+    load_stats lstats;
 
     // events
     cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
@@ -199,13 +328,12 @@ struct pipeline::impl {
     std::vector<cudaEvent_t> comp_ev;        // per outgoing message
     size_t comp_used = 0;
     bool timed_out = false;
-    std::vector<cudaEvent_t> op_ev[2];       // instrumented unit per phase
-    std::vector<cudaEvent_t> lay_ev[2];      // whole layer (LN + 4 ops), same unit
+    std::vector<cudaEvent_t> op_ev[2];       // instrumented unit per phase: 4 ops + attention
+    std::vector<cudaEvent_t> lay_ev[2];      // whole layer, same unit
     std::vector<double> layer_s[2];          // last instrumented run, per layer
     int instr_unit[2] = {-1, -1};
-    kernel_stats kstats[2];
+    kernel_stats kstats[4];
     std::vector<double> unit_s;
-    int launches_per_round = 0;
 
     void* alloc(size_t bytes) {
         void* p = nullptr;
@@ -217,6 +345,139 @@ struct pipeline::impl {
     void* prefill_ptr(int k) const {
         return static_cast<char*>(prompt) + static_cast<size_t>(k) * eta * s * h1 * 2;
     }
+    void* kcache(const layer& L) const { return L.kv; }
+    void* vcache(const layer& L) const {
+        return static_cast<char*>(L.kv) + static_cast<size_t>(B) * S_max * h1 * 2;
+    }
+
+    // ---- weights -----------------------------------------------------------
+    const tensor_source* source(const std::vector<tensor_source>& v, size_t i) const {
+        if (!opt.weights || i >= v.size() || v[i].empty()) return nullptr;
+        return &v[i];
+    }
+    const tensor_source* source(const tensor_source& t) const {
+        return opt.weights && !t.empty() ? &t : nullptr;
+    }
+
+    // bf16 [n x k] -> packed op (tile layout, K1), from a source (binned) or
+    // the seeded synthetic generator
+    void load_linear(bin_loader& ld, const tensor_source* src, uint64_t seed, int64_t nn,
+                     int64_t kk, int b, opw& w, void* tmp) {
+        const int64_t pb = hp_packed_bytes(nn, kk, b);
+        w.packed = alloc(pb);
+        weight_bytes += pb;
+        if (b != 16) {
+            const int64_t sc = hp_scale_count(nn, kk);
+            w.scale = static_cast<float*>(alloc(sc * 4));
+            weight_bytes += sc * 4;
+            if (opt.scheme == HP_ASYMMETRIC) {
+                w.zero = static_cast<float*>(alloc(sc * 4));
+                weight_bytes += sc * 4;
+            }
+        }
+        w.w = hp_qweight{nn, kk, b, opt.scheme, w.packed, w.scale, w.zero};
+        if (!src) {
+            cuda_ok(hp::launch_synth(tmp, nn * kk, seed, 0.0, opt.weight_std, cs), "synth weights");
+            hp_ok(hp_quant_pack(tmp, nn, kk, kk, b, opt.scheme, HP_NEAREST, w.packed, w.scale,
+                                w.zero, nullptr, nullptr, cs),
+                  "quant_pack");
+            return;
+        }
+        // bins of whole 128-row tiles: a row block's codes/scales are
+        // contiguous in the tile layout (layout.cuh)
+        const int64_t G = (kk + 127) / 128;
+        int64_t rows = ld.bin_bytes() / (kk * 2) / 128 * 128;
+        if (rows < 128) throw std::invalid_argument("pipeline: bin_bytes below one 128-row block");
+        for (int64_t r0 = 0; r0 < nn; r0 += rows) {
+            const int64_t rr = std::min(rows, nn - r0);
+            void* bin = ld.fetch(*src, r0 * kk * 2, rr * kk * 2);
+            const int64_t t0 = r0 / 128;
+            hp_ok(hp_quant_pack(bin, rr, kk, kk, b, opt.scheme, HP_NEAREST,
+                                static_cast<char*>(w.packed) + t0 * G * b * 2048,
+                                w.scale ? w.scale + t0 * G * 128 : nullptr,
+                                w.zero ? w.zero + t0 * G * 128 : nullptr, nullptr, nullptr, cs),
+                  "quant_pack (bin)");
+            ld.release();
+        }
+    }
+    // plain bf16 tensor [elems] -> device
+    void* load_plain(bin_loader& ld, const tensor_source* src, uint64_t seed, int64_t elems,
+                     double mean, double std_) {
+        void* d = alloc(elems * 2);
+        weight_bytes += elems * 2;
+        if (!src) {
+            cuda_ok(hp::launch_synth(d, elems, seed, mean, std_, cs), "synth");
+            return d;
+        }
+        for (int64_t off = 0; off < elems * 2; off += ld.bin_bytes()) {
+            const int64_t len = std::min<int64_t>(ld.bin_bytes(), elems * 2 - off);
+            void* bin = ld.fetch(*src, off, len);
+            cuda_ok(cudaMemcpyAsync(static_cast<char*>(d) + off, bin, len, cudaMemcpyDeviceToDevice, cs),
+                    "loader d2d");
+            ld.release();
+        }
+        return d;
+    }
+
+    void load_weights() {
+        const auto t0 = std::chrono::steady_clock::now();
+        const op_shape shp[4] = {{3 * h1, h1}, {h1, h1}, {h2, h1}, {h1, h2}};
+        const int64_t bin = opt.weights ? std::max<int64_t>(opt.weights->bin_bytes, 1 << 20) : (64 << 20);
+        bin_loader ld(cs, bin);
+        void* tmp = alloc(static_cast<size_t>(h2) * h1 * 2);  // synthetic staging (largest op)
+        const std::vector<tensor_source> none;
+        const auto& lin = opt.weights ? opt.weights->linear : none;
+        const auto& nrm = opt.weights ? opt.weights->norm : none;
+        layers.resize(end - begin);
+        for (int l = begin; l < end; ++l) {
+            layer& L = layers[l - begin];
+            L.bits = bits[l - begin];
+            for (int o = 0; o < 4; ++o)
+                load_linear(ld, source(lin, static_cast<size_t>(l) * 4 + o),
+                            seed_for(opt.seed, {1, uint64_t(l), uint64_t(o)}), shp[o].n, shp[o].k,
+                            L.bits, L.ops[o], tmp);
+            for (int j = 0; j < 4; ++j)  // LN gain ~ 1, bias ~ 0 (synthetic)
+                L.ln[j] = load_plain(ld, source(nrm, static_cast<size_t>(l) * 4 + j),
+                                     seed_for(opt.seed, {4, uint64_t(l), uint64_t(j)}), h1,
+                                     (j % 2 == 0) ? 1.0 : 0.0, 0.02);
+            L.kv = alloc(static_cast<size_t>(2) * B * S_max * h1 * 2);
+        }
+        if (first || last) {
+            const tensor_source* es = opt.weights ? source(opt.weights->embed) : nullptr;
+            embed = load_plain(ld, es, seed_for(opt.seed, {6}), vocab * h1, 0.0, 0.02);
+        }
+        if (first && model.pos_s > 2) {
+            const tensor_source* ps = opt.weights ? source(opt.weights->pos) : nullptr;
+            pos_emb = load_plain(ld, ps, seed_for(opt.seed, {7}), model.pos_s * h1, 0.0, 0.02);
+        }
+        if (last) {
+            for (int j = 0; j < 2; ++j) {
+                const tensor_source* fs = opt.weights ? source(opt.weights->final_norm[j]) : nullptr;
+                lnf[j] = load_plain(ld, fs, seed_for(opt.seed, {8, uint64_t(j)}), h1, j == 0 ? 1.0 : 0.0,
+                                    0.02);
+            }
+            // tied LM head: the embedding repacked by K1 at 16 bits (tile layout)
+            const int64_t pb = hp_packed_bytes(vocab, h1, 16);
+            lm.packed = alloc(pb);
+            weight_bytes += pb;
+            lm.w = hp_qweight{vocab, h1, 16, opt.scheme, lm.packed, nullptr, nullptr};
+            hp_ok(hp_quant_pack(embed, vocab, h1, h1, 16, opt.scheme, HP_NEAREST, lm.packed, nullptr,
+                                nullptr, nullptr, nullptr, cs),
+                  "lm head pack");
+            if (!first) {  // the last rank keeps only the packed copy
+                cuda_ok(cudaStreamSynchronize(cs), "lm head");
+                cudaFree(embed);
+                weight_bytes -= vocab * h1 * 2;
+                embed = nullptr;
+            }
+        }
+        cuda_ok(cudaStreamSynchronize(cs), "weights");
+        cudaFree(tmp);
+        lstats.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        lstats.source_bytes = ld.source_bytes();
+        lstats.bins = ld.bins();
+        lstats.packed_bytes = static_cast<double>(weight_bytes);
+    }
 
     void build(const std::vector<std::array<char, 128>>& ids) {
         const auto slice = plan_io::slice_for_stage(plan, rank);
@@ -226,10 +487,22 @@ struct pipeline::impl {
         B = plan.load.global_bz;
         s = plan.load.prompt_len;
         n = plan.load.gen_len;
+        S_max = s + n;
         eta = plan.p.eta;
         xi = plan.p.xi;
         h1 = model.h1;
         h2 = model.h2;
+        vocab = model.vocab_s;
+        heads = model.num_heads;
+        first = rank == 0;
+        last = rank == world - 1;
+        if (heads <= 0 || h1 % heads) throw std::invalid_argument("pipeline: h1 % num_heads != 0");
+        hd = static_cast<int>(h1 / heads);
+        if (hd != 64 && hd != 128)
+            throw std::invalid_argument("pipeline: attention head dim must be 64 or 128 (h1 / num_heads = " +
+                                        std::to_string(hd) + ")");
+        if (S_max > 1024) throw std::invalid_argument("pipeline: s + n must be <= 1024");
+        if (vocab <= 0 || vocab > (int64_t(1) << 31)) throw std::invalid_argument("pipeline: bad vocab_s");
         sched = pipesim::make_schedule(B, eta, xi);
         for (int g = 0; g < sched.num_groups; ++g) {
             group_first.push_back(g * xi);
@@ -270,53 +543,26 @@ struct pipeline::impl {
             nccl_ok(ncclGroupEnd(), "group end");
         }
 
-        // ---- weights: synthetic bf16 generated on device, packed by K1 ------
-        const op_shape shp[4] = {{3 * h1, h1}, {h1, h1}, {h2, h1}, {h1, h2}};
-        void* tmp = alloc(static_cast<size_t>(h2) * h1 * 2);
-        layers.resize(end - begin);
-        for (int l = begin; l < end; ++l) {
-            layer& L = layers[l - begin];
-            L.bits = bits[l - begin];
-            for (int o = 0; o < 4; ++o) {
-                opw& w = L.ops[o];
-                const int64_t nn = shp[o].n, kk = shp[o].k;
-                cuda_ok(hp::launch_synth(tmp, nn * kk, seed_for(opt.seed, {1, uint64_t(l), uint64_t(o)}),
-                                         0.0, opt.weight_std, cs),
-                        "synth weights");
-                const int64_t pb = hp_packed_bytes(nn, kk, L.bits);
-                w.packed = alloc(pb);
-                weight_bytes += pb;
-                if (L.bits != 16) {
-                    const int64_t sc = hp_scale_count(nn, kk);
-                    w.scale = static_cast<float*>(alloc(sc * 4));
-                    weight_bytes += sc * 4;
-                    if (opt.scheme == HP_ASYMMETRIC) {
-                        w.zero = static_cast<float*>(alloc(sc * 4));
-                        weight_bytes += sc * 4;
-                    }
-                }
-                hp_ok(hp_quant_pack(tmp, nn, kk, kk, L.bits, opt.scheme, HP_NEAREST, w.packed,
-                                    w.scale, w.zero, nullptr, nullptr, cs),
-                      "quant_pack");
-                w.w = hp_qweight{nn, kk, L.bits, opt.scheme, w.packed, w.scale, w.zero};
-            }
-            for (int j = 0; j < 4; ++j) {  // LN gain ~ 1, bias ~ 0 (synthetic)
-                L.ln[j] = alloc(h1 * 2);
-                cuda_ok(hp::launch_synth(L.ln[j], h1, seed_for(opt.seed, {4, uint64_t(l), uint64_t(j)}),
-                                         (j % 2 == 0) ? 1.0 : 0.0, 0.02, cs),
-                        "synth ln");
-            }
-        }
-        cuda_ok(cudaStreamSynchronize(cs), "weights");
-        cudaFree(tmp);
+        load_weights();
 
-        // ---- activations -------------------------------------------------
+        // ---- activations and token buffers -----------------------------
         const int64_t M = static_cast<int64_t>(eta) * s;
         prompt = alloc(static_cast<size_t>(B) * s * h1 * 2);
-        if (rank == 0) {
-            pristine = alloc(static_cast<size_t>(B) * s * h1 * 2);
-            cuda_ok(hp::launch_synth(pristine, int64_t(B) * s * h1, seed_for(opt.seed, {3}), 0.0, 1.0, cs),
+        if (first) {
+            prompt_tok = static_cast<int32_t*>(alloc(static_cast<size_t>(B) * s * 4));
+            pristine_tok = static_cast<int32_t*>(alloc(static_cast<size_t>(B) * s * 4));
+            cuda_ok(hp::launch_synth_tokens(pristine_tok, int64_t(B) * s, seed_for(opt.seed, {3}), vocab, cs),
                     "synth prompt");
+        }
+        if (first || last) {
+            cur_tok = static_cast<int32_t*>(alloc(static_cast<size_t>(B) * 4));
+            cuda_ok(cudaMemsetAsync(cur_tok, 0, static_cast<size_t>(B) * 4, cs), "memset");
+        }
+        if (last) {
+            out_tok = static_cast<int32_t*>(alloc(static_cast<size_t>(B) * n * 4));
+            lm_x = alloc(static_cast<size_t>(xi) * h1 * 2);
+            lm_a = alloc(static_cast<size_t>(xi) * h1 * 2);
+            logits = alloc(static_cast<size_t>(xi) * vocab * 2);
         }
         const int64_t Mx = std::max<int64_t>(M, xi);
         scr_a = alloc(Mx * h1 * 2);
@@ -325,38 +571,23 @@ struct pipeline::impl {
         for (int g = 0; g < sched.num_groups; ++g) {
             dec_x.push_back(alloc(static_cast<size_t>(group_size[g]) * h1 * 2));
             cuda_ok(cudaMemsetAsync(dec_x.back(), 0, group_size[g] * h1 * 2, cs), "memset");
-            if (world > 1 && rank == world - 1)
-                fb.push_back(alloc(static_cast<size_t>(group_size[g]) * h1 * 2));
         }
         // split-K workspace: max over this stage's ops and every (rows, phase)
         // the round launches -- a ragged last prefill micro-batch (B % eta != 0)
         // or a short last decode group can need MORE stream-K workspace than
         // the full-size one (fewer tiles -> more segments per tile)
-        for (const auto& sh : round_shapes())
+        for (const auto& sh : round_shapes()) {
             for (const layer& L : layers)
                 for (const opw& w : L.ops)
                     ws_bytes = std::max(ws_bytes,
                                         hp_qlinear_workspace_bytes(&w.w, sh.first, sh.second));
+        }
+        if (last)
+            for (int m = 1; m <= xi; ++m)
+                ws_bytes = std::max(ws_bytes, hp_qlinear_workspace_bytes(&lm.w, m, HP_DECODE));
         if (ws_bytes) {
             ws = alloc(ws_bytes);
             cuda_ok(cudaMemsetAsync(ws, 0, ws_bytes, cs), "ws");
-        }
-
-        if (opt.decode_fused) {
-            std::vector<hp_decoder_layer> dl(layers.size());
-            for (size_t li = 0; li < layers.size(); ++li) {
-                for (int o = 0; o < 4; ++o) dl[li].ops[o] = layers[li].ops[o].w;
-                for (int j = 0; j < 4; ++j) dl[li].ln[j] = layers[li].ln[j];
-                if (li == 0 || layers[li].bits != layers[li - 1].bits) ++dplan_runs;
-            }
-            for (int g = 0; g < sched.num_groups; ++g) {
-                hp_decode_plan* dp = nullptr;
-                hp_ok(hp_decode_plan_create(dl.data(), static_cast<int>(dl.size()), dec_x[g],
-                                            group_size[g], &dp),
-                      "decode_plan_create");
-                dplans.push_back(dp);
-            }
-            for (cudaEvent_t* e : {&dec_ev[0], &dec_ev[1]}) cuda_ok(cudaEventCreate(e), "ev");
         }
 
         load_kernels();
@@ -383,7 +614,7 @@ struct pipeline::impl {
                 instr_unit[1] = static_cast<int>(u);
         }
         for (int ph = 0; ph < 2; ++ph) {
-            op_ev[ph].resize(static_cast<size_t>(layers.size()) * 4 * 2);
+            op_ev[ph].resize(static_cast<size_t>(layers.size()) * 5 * 2);
             for (auto& e : op_ev[ph]) cuda_ok(cudaEventCreate(&e), "ev");
             lay_ev[ph].resize(static_cast<size_t>(layers.size()) * 2);
             for (auto& e : lay_ev[ph]) cuda_ok(cudaEventCreate(&e), "ev");
@@ -392,7 +623,7 @@ struct pipeline::impl {
         cuda_ok(cudaStreamSynchronize(cs), "init");
     }
 
-    // feedback messages last -> 0, in the last stage's emission order
+    // feedback messages last -> 0 (token ids), in the last stage's emission order
     std::vector<unit_ref> feedback_order() const {
         std::vector<unit_ref> out;
         if (world == 1) return out;
@@ -409,49 +640,89 @@ struct pipeline::impl {
         return out;
     }
 
-    void qlin(const opw& w, const void* x, int64_t ldx, int64_t m, void* y, int64_t ldy,
-              const void* res, int epi, int phase, cudaEvent_t* evs) {
-        if (evs) cuda_ok(timing_record(evs[0], cs), "ev");
-        hp_ok(hp_qlinear(&w.w, x, ldx, m, y, ldy, res, res ? ldy : 0, epi, phase, ws, ws_bytes,
-                         cs),
-              "qlinear");
-        if (evs) cuda_ok(timing_record(evs[1], cs), "ev");
+    void record(cudaEvent_t* evs, int i) {
+        if (evs) cuda_ok(timing_record(evs[i], cs), "ev");
     }
 
-    // forward of this stage's layers, in place on x [m x h1]; a decode unit
-    // of group g >= 0 runs the group's K3-fused plan (bound to dec_x[g])
-    void forward(void* x, int64_t m, int phase, bool instrument, int group = -1) {
-        if (phase == HP_DECODE && group >= 0 && !dplans.empty()) {
-            if (instrument) cuda_ok(timing_record(dec_ev[0], cs), "ev");
-            hp_ok(hp_decode_plan_run(dplans[group], cs), "decode_plan_run");
-            if (instrument) cuda_ok(timing_record(dec_ev[1], cs), "ev");
-            return;
-        }
+    void qlin(const opw& w, const void* x, int64_t ldx, int64_t m, void* y, int64_t ldy,
+              const void* res, int epi, int phase) {
+        hp_ok(hp_qlinear(&w.w, x, ldx, m, y, ldy, res, res ? ldy : 0, epi, phase, ws, ws_bytes, cs),
+              "qlinear");
+    }
+
+    // the requests / positions a unit works on (attention context)
+    struct unit_ctx {
+        int req0, nreq;
+        int pos;  // decode: the new token's position; prefill: -1 (positions 0..s-1)
+    };
+
+    // forward of this stage's layers, in place on x [m x h1]
+    void forward(void* x, int64_t m, int phase, bool instrument, const unit_ctx& u) {
         for (size_t li = 0; li < layers.size(); ++li) {
             const layer& L = layers[li];
-            cudaEvent_t* ev = instrument ? &op_ev[phase][li * 8] : nullptr;
+            cudaEvent_t* ev = instrument ? &op_ev[phase][li * 10] : nullptr;
             if (instrument) cuda_ok(timing_record(lay_ev[phase][2 * li], cs), "ev");
             cuda_ok(hp::launch_layernorm(x, h1, m, static_cast<int>(h1), L.ln[0], L.ln[1], scr_a,
                                          h1, cs),
                     "ln1");
-            qlin(L.ops[0], scr_a, h1, m, scr_qkv, 3 * h1, nullptr, HP_EPI_NONE, phase, ev);
-            // self-only attention: output = V slice of qkv
-            qlin(L.ops[1], static_cast<char*>(scr_qkv) + 2 * h1 * 2, 3 * h1, m, x, h1, x,
-                 HP_EPI_NONE, phase, ev ? ev + 2 : nullptr);
+            record(ev, 0);
+            qlin(L.ops[0], scr_a, h1, m, scr_qkv, 3 * h1, nullptr, HP_EPI_NONE, phase);
+            record(ev, 1);
+            // causal multi-head attention over the KV cache -> scr_a
+            if (phase == HP_PREFILL) {
+                cuda_ok(hp::launch_attn_prefill(scr_qkv, u.nreq, s, static_cast<int>(h1), hd, scr_a,
+                                                kcache(L), vcache(L), u.req0, S_max, cs),
+                        "attention (prefill)");
+            } else {
+                cuda_ok(hp::launch_attn_decode(scr_qkv, u.nreq, static_cast<int>(h1), hd, u.pos, scr_a,
+                                               kcache(L), vcache(L), u.req0, S_max, cs),
+                        "attention (decode)");
+            }
+            record(ev, 8);
+            record(ev, 2);
+            qlin(L.ops[1], scr_a, h1, m, x, h1, x, HP_EPI_NONE, phase);
+            record(ev, 3);
             cuda_ok(hp::launch_layernorm(x, h1, m, static_cast<int>(h1), L.ln[2], L.ln[3], scr_a,
                                          h1, cs),
                     "ln2");
-            qlin(L.ops[2], scr_a, h1, m, scr_f, h2, nullptr, HP_EPI_RELU, phase, ev ? ev + 4 : nullptr);
-            qlin(L.ops[3], scr_f, h2, m, x, h1, x, HP_EPI_NONE, phase, ev ? ev + 6 : nullptr);
+            record(ev, 4);
+            qlin(L.ops[2], scr_a, h1, m, scr_f, h2, nullptr, HP_EPI_RELU, phase);
+            record(ev, 5);
+            record(ev, 6);
+            qlin(L.ops[3], scr_f, h2, m, x, h1, x, HP_EPI_NONE, phase);
+            record(ev, 7);
             if (instrument) cuda_ok(timing_record(lay_ev[phase][2 * li + 1], cs), "ev");
         }
     }
+    // attention span of the instrumented layer: events 1 (after qkv) .. 8
+    // (after attention); op spans: (0,1) qkv, (2,3) out, (4,5) fc1, (6,7) fc2
 
-    // CUDA loads a kernel's module lazily at its first launch, and that load
-    // waits for the device: issued while an NCCL recv kernel spins on rs (it
-    // waits for a message this very stage must first compute and send) it
-    // never returns. So run every (phase, rows) forward the round will use,
-    // plus the gather, once on scratch before any NCCL operation is posted.
+    // stage 0: token ids -> x (token embedding + learned position)
+    void embed_prefill(int k) {
+        cuda_ok(hp::launch_embed(prompt_tok + static_cast<size_t>(k) * eta * s, prefill_rows(k), 0, 1, s,
+                                 embed, pos_emb, static_cast<int>(model.pos_s), static_cast<int>(h1),
+                                 vocab, prefill_ptr(k), cs),
+                "embed");
+    }
+    void embed_decode(int g, int tok) {
+        cuda_ok(hp::launch_embed(cur_tok + group_first[g], group_size[g], s + tok - 1, 0, 1, embed, pos_emb,
+                                 static_cast<int>(model.pos_s), static_cast<int>(h1), vocab, dec_x[g], cs),
+                "embed");
+    }
+    // last stage: final LN + tied LM head + argmax of `rows` hidden rows at
+    // x (row stride ldx, first row offset `off`), requests req0.. -> cur_tok
+    // and out_tok[:, col]
+    void lm_head(const void* x, int64_t stride, int64_t off, int rows, int req0, int col) {
+        cuda_ok(hp::launch_gather_rows(x, h1, stride, off, rows, static_cast<int>(h1), lm_x, h1, cs),
+                "gather");
+        cuda_ok(hp::launch_layernorm(lm_x, h1, rows, static_cast<int>(h1), lnf[0], lnf[1], lm_a, h1, cs),
+                "final ln");
+        qlin(lm, lm_a, h1, rows, logits, vocab, nullptr, HP_EPI_NONE, HP_DECODE);
+        cuda_ok(hp::launch_argmax(logits, vocab, rows, vocab, cur_tok + req0,
+                                  out_tok + static_cast<size_t>(req0) * n + col, n, cs),
+                "argmax");
+    }
+
     // every distinct (rows, phase) the round's units run with
     std::vector<std::pair<int64_t, int>> round_shapes() const {
         std::vector<std::pair<int64_t, int>> shapes;
@@ -463,26 +734,35 @@ struct pipeline::impl {
         return shapes;
     }
 
+    // CUDA loads a kernel's module lazily at its first launch, and that load
+    // waits for the device: issued while an NCCL recv kernel spins on rs (it
+    // waits for a message this very stage must first compute and send) it
+    // never returns. So run every (phase, rows) forward the round will use,
+    // and the glue, once on scratch before any NCCL operation is posted.
     void load_kernels() {
         const auto shapes = round_shapes();
         int64_t rows = 1;
         for (const auto& sh : shapes) rows = std::max(rows, sh.first);
         void* x = nullptr;
-        cuda_ok(cudaMalloc(&x, static_cast<size_t>(rows) * h1 * 2 * 2), "cudaMalloc scratch");
+        cuda_ok(cudaMalloc(&x, static_cast<size_t>(rows) * h1 * 2), "cudaMalloc scratch");
         cuda_ok(hp::launch_synth(x, rows * h1, seed_for(opt.seed, {5}), 0.0, 1.0, cs), "synth scratch");
-        for (const auto& sh : shapes) forward(x, sh.first, sh.second, false);
-        for (int g = 0; g < static_cast<int>(dplans.size()); ++g) {
-            forward(dec_x[g], group_size[g], HP_DECODE, false, g);
-            cuda_ok(cudaMemsetAsync(dec_x[g], 0, static_cast<size_t>(group_size[g]) * h1 * 2, cs),
-                    "memset");
+        for (const auto& sh : shapes) {
+            const bool pre = sh.second == HP_PREFILL;
+            forward(x, sh.first, sh.second, false, {0, pre ? static_cast<int>(sh.first / s) : static_cast<int>(sh.first), pre ? -1 : s});
         }
-        cuda_ok(hp::launch_gather_rows(x, h1, 1, 0, 1, static_cast<int>(h1),
-                                       static_cast<char*>(x) + static_cast<size_t>(rows) * h1 * 2, h1,
-                                       cs),
-                "gather");
+        if (first) embed_decode(0, 1);
+        if (last) {
+            for (int g = 0; g < sched.num_groups; ++g) lm_head(x, 1, 0, group_size[g], 0, 0);
+            for (int k = 0; k < static_cast<int>(sched.prefill_sizes.size()); ++k)
+                lm_head(x, 1, 0, sched.prefill_sizes[k], 0, 0);
+        }
         cuda_ok(cudaStreamSynchronize(cs), "load kernels");
         cuda_ok(cudaFree(x), "cudaFree scratch");
         if (ws_bytes) cuda_ok(cudaMemsetAsync(ws, 0, ws_bytes, cs), "ws");
+        if (cur_tok) cuda_ok(cudaMemsetAsync(cur_tok, 0, static_cast<size_t>(B) * 4, cs), "memset");
+        for (const layer& L : layers)  // scratch forwards wrote cache rows
+            cuda_ok(cudaMemsetAsync(L.kv, 0, static_cast<size_t>(2) * B * S_max * h1 * 2, cs), "kv");
+        cuda_ok(cudaStreamSynchronize(cs), "load kernels");
     }
 
     // NCCL connects P2P channels lazily, host-blocking, on the first
@@ -493,31 +773,36 @@ struct pipeline::impl {
     // exchange one message of every size the round uses on each link here,
     // in ascending link order (rank r: link r-1 then link r; rank 0: link 0
     // then link world-1) -- a chain, which cannot deadlock.
-    std::vector<size_t> link_counts(int l) const {
-        std::vector<size_t> c;
+    // Messages: bf16 activations on links l < world-1; int32 token ids on
+    // the feedback link world-1 -> 0. Returns (count, is_tokens).
+    std::vector<std::pair<size_t, bool>> link_msgs(int l) const {
+        std::vector<std::pair<size_t, bool>> c;
         if (l < world - 1) {
             for (int k = 0; k < static_cast<int>(sched.prefill_sizes.size()); ++k)
-                c.push_back(static_cast<size_t>(prefill_rows(k)) * h1);
+                c.push_back({static_cast<size_t>(prefill_rows(k)) * h1, false});
+            for (int g = 0; g < sched.num_groups; ++g) c.push_back({static_cast<size_t>(group_size[g]) * h1, false});
+        } else {
+            for (int g = 0; g < sched.num_groups; ++g) c.push_back({static_cast<size_t>(group_size[g]), true});
         }
-        for (int g = 0; g < sched.num_groups; ++g) c.push_back(static_cast<size_t>(group_size[g]) * h1);
         std::sort(c.begin(), c.end());
         c.erase(std::unique(c.begin(), c.end()), c.end());
         return c;
     }
     void connect_links() {
         const int prev = (rank - 1 + world) % world;
-        size_t maxc = 0;
+        size_t maxb = 0;
         for (int l : {rank, prev})
-            for (size_t c : link_counts(l)) maxc = std::max(maxc, c);
+            for (const auto& c : link_msgs(l)) maxb = std::max(maxb, c.first * (c.second ? 4 : 2));
         void* probe = nullptr;
-        cuda_ok(cudaMalloc(&probe, maxc * 2), "cudaMalloc probe");
+        cuda_ok(cudaMalloc(&probe, maxb), "cudaMalloc probe");
         auto link = [&](bool out) {
-            for (size_t c : link_counts(out ? rank : prev)) {
-                PDBG("connect %s count %zu", out ? "out" : "in", c);
+            for (const auto& c : link_msgs(out ? rank : prev)) {
+                const ncclDataType_t t = c.second ? ncclInt32 : ncclBfloat16;
+                PDBG("connect %s count %zu", out ? "out" : "in", c.first);
                 if (out)
-                    nccl_ok(ncclSend(probe, c, ncclBfloat16, /*peer=*/1, c_out, cs), "connect send");
+                    nccl_ok(ncclSend(probe, c.first, t, /*peer=*/1, c_out, cs), "connect send");
                 else
-                    nccl_ok(ncclRecv(probe, c, ncclBfloat16, /*peer=*/0, c_in, cs), "connect recv");
+                    nccl_ok(ncclRecv(probe, c.first, t, /*peer=*/0, c_in, cs), "connect recv");
                 cuda_ok(cudaStreamSynchronize(cs), "connect");
             }
         };
@@ -531,6 +816,12 @@ struct pipeline::impl {
         cuda_ok(cudaFree(probe), "cudaFree probe");
     }
 
+    void send_after_compute(const void* buf, size_t count, ncclDataType_t t, int& comp_i) {
+        cuda_ok(cudaEventRecord(comp_ev[comp_i], cs), "ev");
+        cuda_ok(cudaStreamWaitEvent(ss, comp_ev[comp_i++], 0), "wait");
+        nccl_ok(ncclSend(buf, count, t, /*peer=*/1, c_out, ss), "send");
+    }
+
     // Enqueue one whole round on (cs, ss, rs). Capturable.
     void enqueue_round() {
         // fork side streams off the compute stream (joins them into a capture)
@@ -539,36 +830,32 @@ struct pipeline::impl {
         cuda_ok(cudaStreamWaitEvent(rs, ev_fork, 0), "wait");
 
         // post every receive in the sender's order
+        std::map<std::tuple<int, int, int>, int> recv_idx;
         if (world > 1) {
             const std::vector<unit_ref> incoming = rank > 0 ? prev_units : feedback_order();
             for (size_t i = 0; i < incoming.size(); ++i) {
                 const unit_ref& u = incoming[i];
-                void* dst;
-                size_t count;
+                PDBG("recv %zu (kind %d idx %d tok %d)", i, static_cast<int>(u.kind), u.index, u.token);
                 if (rank > 0 && u.kind == pipesim::unit_kind::prefill) {
-                    dst = prefill_ptr(u.index);
-                    count = static_cast<size_t>(prefill_rows(u.index)) * h1;
-                } else {
-                    dst = dec_x[u.index];
-                    count = static_cast<size_t>(group_size[u.index]) * h1;
+                    nccl_ok(ncclRecv(prefill_ptr(u.index), static_cast<size_t>(prefill_rows(u.index)) * h1,
+                                     ncclBfloat16, /*peer=*/0, c_in, rs),
+                            "recv");
+                } else if (rank > 0) {
+                    nccl_ok(ncclRecv(dec_x[u.index], static_cast<size_t>(group_size[u.index]) * h1,
+                                     ncclBfloat16, /*peer=*/0, c_in, rs),
+                            "recv");
+                } else {  // stage 0: the group's next token ids from the last stage
+                    nccl_ok(ncclRecv(cur_tok + group_first[u.index], static_cast<size_t>(group_size[u.index]),
+                                     ncclInt32, /*peer=*/0, c_in, rs),
+                            "recv tokens");
                 }
-                PDBG("recv %zu (kind %d idx %d tok %d) count %zu", i, static_cast<int>(u.kind), u.index, u.token, count);
-                nccl_ok(ncclRecv(dst, count, ncclBfloat16, /*peer=*/0, c_in, rs), "recv");
                 cuda_ok(cudaEventRecord(recv_ev[i], rs), "ev");
+                recv_idx[{static_cast<int>(u.kind), u.index, u.token}] = static_cast<int>(i);
             }
-        }
-        // map unit -> its recv index
-        std::map<std::tuple<int, int, int>, int> recv_idx;
-        if (world > 1) {
-            const std::vector<unit_ref> incoming = rank > 0 ? prev_units : feedback_order();
-            for (size_t i = 0; i < incoming.size(); ++i)
-                recv_idx[{static_cast<int>(incoming[i].kind), incoming[i].index,
-                          incoming[i].token}] = static_cast<int>(i);
         }
         std::vector<int> left(sched.num_groups, 0);
         for (int g : sched.group_of_prefill) ++left[g];
         int comp_i = 0;
-        const bool last = rank == world - 1;
 
         for (size_t ui = 0; ui < units.size(); ++ui) {
             const unit_ref& u = units[ui];
@@ -584,59 +871,37 @@ struct pipeline::impl {
             void* x = pre ? prefill_ptr(u.index) : dec_x[u.index];
             const int64_t m = pre ? prefill_rows(u.index) : group_size[u.index];
             const int phase = pre ? HP_PREFILL : HP_DECODE;
+            const unit_ctx ctx = pre ? unit_ctx{u.index * eta, sched.prefill_sizes[u.index], -1}
+                                     : unit_ctx{group_first[u.index], group_size[u.index], s + u.token - 1};
             cuda_ok(timing_record(unit_ev[2 * ui], cs), "ev");
-            forward(x, m, phase, opt.instrument && instr_unit[phase] == static_cast<int>(ui),
-                    pre ? -1 : u.index);
+            if (first) {
+                if (pre) embed_prefill(u.index);
+                else embed_decode(u.index, u.token);
+            }
+            forward(x, m, phase, opt.instrument && instr_unit[phase] == static_cast<int>(ui), ctx);
+            if (last) {
+                if (pre) lm_head(x, s, s - 1, sched.prefill_sizes[u.index], ctx.req0, 0);
+                else lm_head(x, 1, 0, group_size[u.index], ctx.req0, u.token);
+            }
             cuda_ok(timing_record(unit_ev[2 * ui + 1], cs), "ev");
 
             // ---- output
             if (!last) {
-                cuda_ok(cudaEventRecord(comp_ev[comp_i], cs), "ev");
-                cuda_ok(cudaStreamWaitEvent(ss, comp_ev[comp_i++], 0), "wait");
                 PDBG("send unit %zu count %zu", ui, static_cast<size_t>(m) * h1);
-                nccl_ok(ncclSend(x, static_cast<size_t>(m) * h1, ncclBfloat16, /*peer=*/1, c_out, ss),
-                        "send");
-                PDBG("send unit %zu posted", ui);
+                send_after_compute(x, static_cast<size_t>(m) * h1, ncclBfloat16, comp_i);
                 continue;
             }
+            if (world == 1) continue;
             if (pre) {
-                // last position of each request -> its decode group's input
                 const int g = sched.group_of_prefill[u.index];
-                const int req0 = u.index * eta;
-                void* dst_base = world > 1 ? fb[g] : dec_x[g];
-                const int row0 = req0 - group_first[g];
-                // a prefill batch may straddle a group boundary: split
-                int r = 0;
-                while (r < sched.prefill_sizes[u.index]) {
-                    const int req = req0 + r;
-                    const int gg = req / xi;
-                    const int take = std::min(sched.prefill_sizes[u.index] - r,
-                                              group_first[gg] + group_size[gg] - req);
-                    void* dst = world > 1 ? fb[gg] : dec_x[gg];
-                    cuda_ok(hp::launch_gather_rows(x, h1, s, static_cast<int64_t>(r) * s + s - 1, take,
-                                                   static_cast<int>(h1),
-                                                   static_cast<char*>(dst) +
-                                                       static_cast<size_t>(req - group_first[gg]) * h1 * 2,
-                                                   h1, cs),
-                            "gather");
-                    r += take;
-                }
-                (void)dst_base;
-                (void)row0;
-                if (--left[g] == 0 && n >= 2 && world > 1) {
-                    cuda_ok(cudaEventRecord(comp_ev[comp_i], cs), "ev");
-                    cuda_ok(cudaStreamWaitEvent(ss, comp_ev[comp_i++], 0), "wait");
-                    PDBG("send fb group %d count %zu", g, static_cast<size_t>(group_size[g]) * h1);
-                    nccl_ok(ncclSend(fb[g], static_cast<size_t>(group_size[g]) * h1, ncclBfloat16,
-                                     /*peer=*/1, c_out, ss),
-                            "send fb");
-                }
-            } else if (world > 1 && u.token + 1 <= n - 1) {
-                cuda_ok(cudaEventRecord(comp_ev[comp_i], cs), "ev");
-                cuda_ok(cudaStreamWaitEvent(ss, comp_ev[comp_i++], 0), "wait");
-                PDBG("send fb unit %zu count %zu", ui, static_cast<size_t>(m) * h1);
-                nccl_ok(ncclSend(x, static_cast<size_t>(m) * h1, ncclBfloat16, /*peer=*/1, c_out, ss),
-                        "send fb");
+                // a prefill batch may straddle a group boundary: its tokens
+                // are complete once the group's last batch is done
+                if (--left[g] == 0 && n >= 2)
+                    send_after_compute(cur_tok + group_first[g], static_cast<size_t>(group_size[g]), ncclInt32,
+                                       comp_i);
+            } else if (u.token + 1 <= n - 1) {
+                send_after_compute(cur_tok + group_first[u.index], static_cast<size_t>(group_size[u.index]),
+                                   ncclInt32, comp_i);
             }
         }
         comp_used = static_cast<size_t>(comp_i);
@@ -695,44 +960,34 @@ struct pipeline::impl {
         graph_ready = true;
     }
 
-    run_timing run(const void* host_prompt, void* host_out) {
+    void load_prompt(const int32_t* host_tokens) {
+        if (!first) return;
+        const size_t bytes = static_cast<size_t>(B) * s * 4;
+        if (host_tokens)
+            cuda_ok(cudaMemcpyAsync(prompt_tok, host_tokens, bytes, cudaMemcpyHostToDevice, cs), "h2d");
+        else
+            cuda_ok(cudaMemcpyAsync(prompt_tok, pristine_tok, bytes, cudaMemcpyDeviceToDevice, cs), "d2d");
+    }
+
+    run_timing run(const int32_t* host_tokens, int32_t* host_out) {
         run_timing t;
         cuda_ok(cudaEventRecord(ev_t0, cs), "ev");
-        if (rank == 0) {
-            const size_t bytes = static_cast<size_t>(B) * s * h1 * 2;
-            if (host_prompt)
-                cuda_ok(cudaMemcpyAsync(prompt, host_prompt, bytes, cudaMemcpyHostToDevice, cs), "h2d");
-            else
-                cuda_ok(cudaMemcpyAsync(prompt, pristine, bytes, cudaMemcpyDeviceToDevice, cs), "d2d");
-        }
+        load_prompt(host_tokens);
         if (opt.use_graphs) {
             if (!graph_ready) {
                 enqueue_round();  // eager warm-up (sets kernel attributes)
                 wait_round("warm-up round");
-                if (rank == 0) {
-                    const size_t bytes = static_cast<size_t>(B) * s * h1 * 2;
-                    cuda_ok(cudaMemcpyAsync(prompt, host_prompt ? host_prompt : pristine, bytes,
-                                            host_prompt ? cudaMemcpyHostToDevice
-                                                        : cudaMemcpyDeviceToDevice,
-                                            cs),
-                            "reload");
-                }
+                load_prompt(host_tokens);
                 capture();
             }
             cuda_ok(cudaGraphLaunch(graph, cs), "graph launch");
         } else {
             enqueue_round();
         }
-        if (rank == world - 1 && host_out) {
-            for (int g = 0; g < sched.num_groups; ++g) {
-                const void* src = (n >= 2 || world == 1) ? dec_x[g] : fb[g];
-                cuda_ok(cudaMemcpyAsync(static_cast<char*>(host_out) +
-                                            static_cast<size_t>(group_first[g]) * h1 * 2,
-                                        src, static_cast<size_t>(group_size[g]) * h1 * 2,
-                                        cudaMemcpyDeviceToHost, cs),
-                        "d2h");
-            }
-        }
+        if (last && host_out)
+            cuda_ok(cudaMemcpyAsync(host_out, out_tok, static_cast<size_t>(B) * n * 4,
+                                    cudaMemcpyDeviceToHost, cs),
+                    "d2h");
         cuda_ok(cudaEventRecord(ev_t1, cs), "ev");
         wait_round("round");
         float ms = 0.f;
@@ -749,41 +1004,33 @@ struct pipeline::impl {
         return t;
     }
 
+    void final_hidden(void* host) const {
+        if (!last) throw std::invalid_argument("pipeline: final_hidden is on the last rank");
+        for (int g = 0; g < sched.num_groups; ++g)
+            cuda_ok(cudaMemcpy(static_cast<char*>(host) + static_cast<size_t>(group_first[g]) * h1 * 2,
+                               n >= 2 ? dec_x[g] : prompt, static_cast<size_t>(group_size[g]) * h1 * 2,
+                               cudaMemcpyDeviceToHost),
+                    "final hidden");
+    }
+
     void collect_kernel_stats() {
         const op_shape shp[4] = {{3 * h1, h1}, {h1, h1}, {h2, h1}, {h1, h2}};
+        const int pairs[4][2] = {{0, 1}, {2, 3}, {4, 5}, {6, 7}};
         for (int ph = 0; ph < 2; ++ph) {
             const int ui = instr_unit[ph];
             if (ui < 0) continue;
             const unit_ref& u = units[ui];
             const int64_t m = ph == 0 ? prefill_rows(u.index) : group_size[u.index];
-            if (ph == 1 && !dplans.empty()) {
-                // K3 fused: one timed span over the unit's launches; per-layer
-                // decode costs need per-op decode (tools/layer_costs.py)
-                float ms = 0.f;
-                cuda_ok(cudaEventElapsedTime(&ms, dec_ev[0], dec_ev[1]), "elapsed fused");
-                double info[4];
-                hp_ok(hp_decode_plan_info(dplans[u.index], info), "decode_plan_info");
-                kernel_stats& k = kstats[1];
-                k.launches += dplan_runs;
-                k.seconds += ms * 1e-3;
-                k.bytes += info[1];
-                for (size_t li = 0; li < layers.size(); ++li) {
-                    layer_s[1][li] = 0.0;
-                    for (int o = 0; o < 4; ++o) k.flops += 2.0 * m * shp[o].n * shp[o].k;
-                }
-                continue;
-            }
+            const int nreq = ph == 0 ? sched.prefill_sizes[u.index] : group_size[u.index];
+            const double ctx = ph == 0 ? s : s + u.token;  // keys per query (decode) / prompt
             for (size_t li = 0; li < layers.size(); ++li) {
                 float ms = 0.f;
                 cuda_ok(cudaEventElapsedTime(&ms, lay_ev[ph][2 * li], lay_ev[ph][2 * li + 1]),
                         "elapsed layer");
                 layer_s[ph][li] = ms * 1e-3;
-            }
-            for (size_t li = 0; li < layers.size(); ++li)
                 for (int o = 0; o < 4; ++o) {
-                    float ms = 0.f;
-                    cuda_ok(cudaEventElapsedTime(&ms, op_ev[ph][li * 8 + 2 * o],
-                                                 op_ev[ph][li * 8 + 2 * o + 1]),
+                    cuda_ok(cudaEventElapsedTime(&ms, op_ev[ph][li * 10 + pairs[o][0]],
+                                                 op_ev[ph][li * 10 + pairs[o][1]]),
                             "elapsed op");
                     kernel_stats& k = kstats[ph];
                     ++k.launches;
@@ -791,6 +1038,19 @@ struct pipeline::impl {
                     k.bytes += k3_bytes(shp[o], layers[li].bits, opt.scheme, m);
                     k.flops += 2.0 * m * shp[o].n * shp[o].k;
                 }
+                cuda_ok(cudaEventElapsedTime(&ms, op_ev[ph][li * 10 + 1], op_ev[ph][li * 10 + 8]),
+                        "elapsed attention");
+                kernel_stats& a = kstats[2 + ph];
+                ++a.launches;
+                a.seconds += ms * 1e-3;
+                if (ph == 0) {  // causal: s(s+1)/2 score rows x hd, QK^T and PV
+                    a.flops += 4.0 * nreq * heads * hd * (static_cast<double>(s) * (s + 1) / 2);
+                    a.bytes += 2.0 * m * 3 * h1 + 2.0 * m * h1 + 2.0 * 2 * m * h1;  // qkv in, out, K/V cache write
+                } else {  // K and V rows 0..p of every request, + qkv in, out
+                    a.bytes += 2.0 * 2 * nreq * ctx * h1 + 2.0 * m * 3 * h1 + 2.0 * m * h1;
+                    a.flops += 4.0 * nreq * heads * hd * ctx;
+                }
+            }
         }
     }
 
@@ -823,18 +1083,13 @@ struct pipeline::impl {
                 f(w.zero);
             }
             for (void* p : L.ln) f(p);
+            f(L.kv);
         }
-        f(prompt);
-        f(pristine);
-        f(scr_a);
-        f(scr_qkv);
-        f(scr_f);
+        for (void* p : {embed, pos_emb, static_cast<void*>(prompt_tok), static_cast<void*>(pristine_tok),
+                        lnf[0], lnf[1], lm.packed, lm_x, lm_a, logits, static_cast<void*>(out_tok),
+                        static_cast<void*>(cur_tok), prompt, scr_a, scr_qkv, scr_f, ws})
+            f(p);
         for (void* p : dec_x) f(p);
-        for (void* p : fb) f(p);
-        f(ws);
-        for (hp_decode_plan* dp : dplans) hp_decode_plan_destroy(dp);
-        for (cudaEvent_t e : dec_ev)
-            if (e) cudaEventDestroy(e);
         for (auto* v : {&unit_ev, &recv_ev, &comp_ev, &op_ev[0], &op_ev[1], &lay_ev[0], &lay_ev[1]})
             for (cudaEvent_t e : *v) cudaEventDestroy(e);
         for (cudaEvent_t e : {ev_t0, ev_t1, ev_fork, ev_join_s, ev_join_r})
@@ -859,19 +1114,28 @@ pipeline::pipeline(const plan_io::plan_document& plan, const model_spec& model, 
         throw std::invalid_argument("pipeline: model/plan layer count mismatch");
     if (world > 1 && static_cast<int>(nccl_ids.size()) < world)
         throw std::invalid_argument("pipeline: need one NCCL id per link");
+    if (opt.weights) {
+        const size_t L4 = static_cast<size_t>(plan.num_layers) * 4;
+        if ((!opt.weights->linear.empty() && opt.weights->linear.size() != L4) ||
+            (!opt.weights->norm.empty() && opt.weights->norm.size() != L4))
+            throw std::invalid_argument("pipeline: weight set needs num_layers*4 linear / norm entries");
+    }
     p_->plan = plan;
     p_->model = model;
     p_->rank = rank;
     p_->world = world;
     p_->opt = opt;
     p_->build(nccl_ids);
+    p_->opt.weights = nullptr;  // the caller's set is read during construction only
 }
 
 pipeline::~pipeline() = default;
 
-run_timing pipeline::run(const void* host_prompt, void* host_out) {
-    return p_->run(host_prompt, host_out);
+run_timing pipeline::run(const std::int32_t* host_tokens, std::int32_t* host_out) {
+    return p_->run(host_tokens, host_out);
 }
+
+void pipeline::final_hidden(void* host) const { p_->final_hidden(host); }
 
 pipesim::stage_cost pipeline::measured_cost() const {
     pipesim::stage_cost c;
@@ -891,28 +1155,29 @@ pipesim::stage_cost pipeline::measured_cost() const {
     return c;
 }
 
-const kernel_stats& pipeline::stats(int phase) const { return p_->kstats[phase ? 1 : 0]; }
+const kernel_stats& pipeline::stats(int kind) const { return p_->kstats[std::clamp(kind, 0, 3)]; }
 
 const std::vector<double>& pipeline::layer_costs(int phase) const {
     return p_->layer_s[phase ? 1 : 0];
 }
 
 void pipeline::reset_stats() {
-    p_->kstats[0] = kernel_stats{};
-    p_->kstats[1] = kernel_stats{};
+    for (auto& k : p_->kstats) k = kernel_stats{};
 }
 
 std::int64_t pipeline::weight_bytes() const { return p_->weight_bytes; }
 
+const load_stats& pipeline::loading() const { return p_->lstats; }
+
 int pipeline::num_kernel_launches_per_round() const {
     int n = 0;
-    for (const unit_ref& u : p_->units)
-        n += (u.kind == pipesim::unit_kind::decode && !p_->dplans.empty())
-                 ? p_->dplan_runs
-                 : static_cast<int>(p_->layers.size()) * 6;
-    if (p_->rank == p_->world - 1)
-        for (const unit_ref& u : p_->units)
-            if (u.kind == pipesim::unit_kind::prefill) ++n;  // gather (>=1)
+    const int per_layer = 7;  // LN1, qkv, attention, out, LN2, fc1, fc2
+    for (const unit_ref& u : p_->units) {
+        n += static_cast<int>(p_->layers.size()) * per_layer;
+        if (p_->first) ++n;                                            // embedding
+        if (p_->last) n += 4;                                          // gather, LN, LM head, argmax
+        (void)u;
+    }
     return n;
 }
 

@@ -171,39 +171,40 @@ def qlinear(qw: QuantizedWeight, x: torch.Tensor, phase: int = capi.HP_DECODE,
     return out
 
 
-class DecodePlan:
-    """K3 fused: one decode step of a decoder-layer stack in one persistent
-    kernel (hp_decode_plan_*). layers: [(qkv, out, fc1, fc2), (ln1_g, ln1_b,
-    ln2_g, ln2_b)] per layer; x [m x h1] bf16 is updated in place by run()."""
+# ---- decoder glue (decoder.cu; hp_embed / hp_attention_* / hp_argmax) ----
+def embed(tok: torch.Tensor, E: torch.Tensor, P: torch.Tensor | None, pos0: int,
+          pos_per_req: bool = False, s_tokens: int = 1, stream=None) -> torch.Tensor:
+    """x[r] = E[tok[r]] + P[pos(r) + 2] (OPT learned positions)."""
+    rows = tok.numel()
+    h = E.shape[1]
+    x = torch.empty(rows, h, dtype=torch.bfloat16, device=E.device)
+    check(lib.hp_embed(tok.data_ptr(), rows, pos0, int(pos_per_req), s_tokens, E.data_ptr(),
+                       _ptr(P), P.shape[0] if P is not None else 0, h, E.shape[0], x.data_ptr(),
+                       _stream(stream)))
+    return x
 
-    def __init__(self, layers, x: torch.Tensor):
-        assert x.dtype == torch.bfloat16 and x.is_cuda and x.is_contiguous()
-        self._keep = (layers, x)
-        arr = (capi.hp_decoder_layer * len(layers))()
-        for i, (ops, lns) in enumerate(layers):
-            for o in range(4):
-                arr[i].ops[o] = ops[o].c
-            for j in range(4):
-                arr[i].ln[j] = lns[j].data_ptr()
-        h = C.c_void_p()
-        check(lib.hp_decode_plan_create(arr, len(layers), x.data_ptr(), x.shape[0], C.byref(h)))
-        self.h = h
 
-    def run(self, stream=None) -> None:
-        check(lib.hp_decode_plan_run(self.h, _stream(stream)))
+def attention_prefill(qkv: torch.Tensor, reqs: int, s: int, hd: int, kc: torch.Tensor,
+                      vc: torch.Tensor, req0: int, s_max: int, stream=None) -> torch.Tensor:
+    h = qkv.shape[1] // 3
+    out = torch.empty(reqs * s, h, dtype=torch.bfloat16, device=qkv.device)
+    check(lib.hp_attention_prefill(qkv.data_ptr(), reqs, s, h, hd, out.data_ptr(), kc.data_ptr(),
+                                   vc.data_ptr(), req0, s_max, _stream(stream)))
+    return out
 
-    def info(self) -> dict:
-        out = (C.c_double * 4)()
-        check(lib.hp_decode_plan_info(self.h, out))
-        return {"weight_bytes": out[0], "alg_bytes": out[1], "ops": int(out[2]), "grid": int(out[3])}
 
-    def close(self) -> None:
-        if self.h:
-            lib.hp_decode_plan_destroy(self.h)
-            self.h = None
+def attention_decode(qkv: torch.Tensor, hd: int, p: int, kc: torch.Tensor, vc: torch.Tensor,
+                     req0: int, s_max: int, stream=None) -> torch.Tensor:
+    rows, h = qkv.shape[0], qkv.shape[1] // 3
+    out = torch.empty(rows, h, dtype=torch.bfloat16, device=qkv.device)
+    check(lib.hp_attention_decode(qkv.data_ptr(), rows, h, hd, p, out.data_ptr(), kc.data_ptr(),
+                                  vc.data_ptr(), req0, s_max, _stream(stream)))
+    return out
 
-    def __del__(self):
-        try:
-            self.close()
-        except Exception:
-            pass
+
+def argmax(logits: torch.Tensor, stream=None) -> torch.Tensor:
+    rows, vocab = logits.shape
+    tok = torch.empty(rows, dtype=torch.int32, device=logits.device)
+    check(lib.hp_argmax(logits.data_ptr(), logits.stride(0), rows, vocab, tok.data_ptr(),
+                        _stream(stream)))
+    return tok

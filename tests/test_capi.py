@@ -26,7 +26,7 @@ def test_every_declared_symbol_is_exported():
 
 
 def test_abi_version_and_sizes():
-    assert capi.lib.hp_abi_version() == 1
+    assert capi.lib.hp_abi_version() == 2
     # packed-size contract (memcost.cpp:15-18): ceil(n*k*b/8) on aligned shapes
     for bits in (3, 4, 8, 16):
         assert capi.lib.hp_packed_bytes(5120, 20480, bits) == 5120 * 20480 * bits // 8

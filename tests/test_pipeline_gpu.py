@@ -1,12 +1,18 @@
-"""End-to-end stage execution on one B200 through the C-ABI pipeline.
+"""End-to-end serving round on one B200 through the C-ABI pipeline (OPT
+decoder: token + position embedding, per layer LN -> qkv -> causal attention
+over the KV cache -> out(+res) -> LN -> fc1(relu) -> fc2(+res), final LN,
+tied LM head, greedy argmax).
 
-The runtime generates its own synthetic weights on the device (mirror of
-oracle/synth.py) and quantizes them with K1; the test rebuilds the same
-layers from oracle/synth.py bits, dequantizes them with the SAME K1 codes
-(hp_quant_pack + hp_dequant) and runs a torch reference forward that rounds
-to bf16 where the runtime stores bf16, so the comparison isolates the
-GEMM accumulation order. Plan: the OPT-125M fixture from the reference
-planner (tests/golden/plans/opt125m_b8_1gpu.json), B=8, s=512.
+Reference: a torch fp32 decoder built on ORACLE-dequantized weights
+(oracle/hp_oracle.c quantize() restatement, zero + (code - off) * step,
+indicator.cpp:53) of the same synthetic checkpoint (oracle/synth.py seeds),
+rounding to bf16 wherever the runtime stores bf16. It is teacher-forced
+with the runtime's generated tokens (one causal pass over prompt + tokens),
+so a near-tie argmax flip cannot derail the comparison: every generated
+token must be the reference's argmax up to a logit margin, and the final
+hidden state of the last position must match within the tolerance.
+Plan: the OPT-125M fixture from the reference planner
+(tests/golden/plans/opt125m_b8_1gpu.json), B=8, s=512.
 """
 import json
 
@@ -17,7 +23,8 @@ from tests.util import bits_to_torch
 
 pytestmark = pytest.mark.gpu
 
-H1, H2 = 768, 3072
+H1, H2, HEADS, VOCAB, POS = 768, 3072, 12, 50272, 2050
+SHAPES = [(3 * H1, H1), (H1, H1), (H2, H1), (H1, H2)]
 
 
 def _plan(n=4):
@@ -28,23 +35,50 @@ def _plan(n=4):
     return plan, model_json
 
 
-def _ref_forward(plan, dev, n):
-    import torch
+def _synth(n, seed, mean, std):
     from oracle import synth
-    from paper_2403_01136_b200 import qweight
-    shapes = [(3 * H1, H1), (H1, H1), (H2, H1), (H1, H2)]
-    layers = []
+    return synth.synth_bits(n, seed, mean, std)
+
+
+def _checkpoint(bits):
+    """bf16 bit patterns of every tensor of the synthetic checkpoint."""
+    from oracle import synth
+    ck = {"linear": [], "norm": []}
+    for i in range(len(bits)):
+        for o, (nn, kk) in enumerate(SHAPES):
+            ck["linear"].append(_synth(nn * kk, synth.seed_for(1, i, o), 0.0, 0.02).reshape(nn, kk))
+        for j in range(4):
+            ck["norm"].append(_synth(H1, synth.seed_for(4, i, j), 1.0 if j % 2 == 0 else 0.0, 0.02))
+    ck["embed"] = _synth(VOCAB * H1, synth.seed_for(6), 0.0, 0.02).reshape(VOCAB, H1)
+    ck["pos"] = _synth(POS * H1, synth.seed_for(7), 0.0, 0.02).reshape(POS, H1)
+    ck["lnf"] = [_synth(H1, synth.seed_for(8, j), 1.0 if j == 0 else 0.0, 0.02) for j in range(2)]
+    return ck
+
+
+def _ref_logits_and_hidden(plan, ck, tokens, dev):
+    """Teacher-forced reference over prompt + generated tokens [B, s + n - 1]."""
+    import torch
+
+    import oracle
+    port = oracle.port()
+    ws = []
     for i, b in enumerate(plan["layer_bits"]):
-        ws = []
-        for o, (nn, kk) in enumerate(shapes):
-            wb = synth.synth_bits(nn * kk, synth.seed_for(1, i, o), 0.0, 0.02).reshape(nn, kk)
-            w = bits_to_torch(wb, dev)
-            ws.append(qweight.dequant(qweight.quantize(w, b)).float() if b != 16 else w.float())
-        ln = [bits_to_torch(synth.synth_bits(H1, synth.seed_for(4, i, j), 1.0 if j % 2 == 0 else 0.0,
-                                             0.02), dev).float() for j in range(4)]
-        layers.append((ws, ln))
-    B, s = plan["workload"]["global_bz"], plan["workload"]["s"]
-    x = bits_to_torch(synth.synth_bits(B * s * H1, synth.seed_for(3), 0.0, 1.0), dev).reshape(B * s, H1)
+        lw = []
+        for o in range(4):
+            wb = ck["linear"][4 * i + o]
+            if b == 16:
+                lw.append(bits_to_torch(wb, dev).float())
+            else:
+                codes, step, zero = port.quantize_matrix(wb, b, 1)
+                off = (1 << (b - 1)) - 1
+                k = wb.shape[1]
+                w = zero.repeat(128, axis=1)[:, :k] + (codes.astype(np.float64) - off) * step.repeat(128, axis=1)[:, :k]
+                lw.append(torch.from_numpy(w).to(dev).float())
+        ln = [bits_to_torch(ck["norm"][4 * i + j], dev).float() for j in range(4)]
+        ws.append((lw, ln))
+    E = bits_to_torch(ck["embed"], dev).float()
+    P = bits_to_torch(ck["pos"], dev).float()
+    lnf = [bits_to_torch(v, dev).float() for v in ck["lnf"]]
 
     def bf(t):
         return t.to(torch.bfloat16).float()
@@ -54,96 +88,180 @@ def _ref_forward(plan, dev, n):
         var = ((x - mu) ** 2).mean(-1, keepdim=True)
         return bf((x - mu) * torch.rsqrt(var + 1e-5) * g + b)
 
-    def stack(x):
-        x = x.float()
-        for ws, ln in layers:
-            a = ln_(x, ln[0], ln[1])
-            qkv = bf(a @ ws[0].T)
-            x = bf(qkv[:, 2 * H1:] @ ws[1].T + x)
-            a = ln_(x, ln[2], ln[3])
-            f = bf(torch.relu(a @ ws[2].T))
-            x = bf(f @ ws[3].T + x)
-        return x
+    tok = torch.from_numpy(tokens).to(dev).long()
+    B, T = tok.shape
+    x = bf(E[tok] + P[torch.arange(T, device=dev) + 2])
+    mask = torch.ones(T, T, dtype=torch.bool, device=dev).tril()
+    for lw, ln in ws:
+        a = ln_(x, ln[0], ln[1])
+        qkv = bf(a @ lw[0].T)
+        q, k, v = (qkv[..., j * H1:(j + 1) * H1].reshape(B, T, HEADS, H1 // HEADS) for j in range(3))
+        sc = torch.einsum("bthd,bshd->bhts", q, k) / np.sqrt(H1 // HEADS)
+        sc = sc.masked_fill(~mask, float("-inf"))
+        att = bf(torch.einsum("bhts,bshd->bthd", torch.softmax(sc, -1), v).reshape(B, T, H1))
+        x = bf(x + att @ lw[1].T)
+        a = ln_(x, ln[2], ln[3])
+        f = bf(torch.relu(a @ lw[2].T))
+        x = bf(x + f @ lw[3].T)
+    logits = bf(ln_(x, lnf[0], lnf[1]) @ E.T)
+    return logits, x
 
-    eta = plan["eta"]
-    outs = []
-    for k in range(0, B, eta):
-        y = stack(x[k * s:(k + eta) * s])
-        outs.append(y.reshape(-1, s, H1)[:, -1])
-    d = torch.cat(outs)
-    for _ in range(n - 1):
-        d = stack(d)
-    return d
+
+def _run(pipe, B, n, host_tokens=None):
+    import torch
+    out = torch.empty(B * n, dtype=torch.int32).pin_memory()
+    pipe.run(host_tokens.data_ptr() if host_tokens is not None else None, out.data_ptr())
+    return out.clone()
+
+
+def _final_hidden(pipe, B):
+    import torch
+    h = torch.empty(B * H1, dtype=torch.bfloat16)
+    pipe.final_hidden(h.data_ptr())
+    return h.reshape(B, H1)
 
 
 @pytest.mark.parametrize("graphs", [True, False])
-def test_opt125m_stage_matches_reference(cuda, graphs):
+def test_opt125m_round_matches_reference_decoder(cuda, graphs):
     import torch
+
+    from oracle import synth
     from paper_2403_01136_b200.pipeline import Pipeline
     n = 4
     plan, model_json = _plan(n)
+    B, s = 8, 512
     pipe = Pipeline(json.dumps(plan), model_json, use_graphs=graphs, instrument=True)
-    out = torch.empty(8 * H1, dtype=torch.bfloat16).pin_memory()
-    t = pipe.run(None, out.data_ptr())
-    t2 = pipe.run(None, out.data_ptr())  # graph replay path when graphs=True
-    assert t.makespan_s > 0 and t2.makespan_s > 0
-    got = out.float().reshape(8, H1)
-    ref = _ref_forward(plan, cuda, n).cpu()
-    assert torch.isfinite(got).all()
-    err = float((got - ref).abs().max() / ref.abs().max())
-    assert err < 2e-2, err
-    ks = pipe.kernel_stats(1)
-    assert ks["launches"] > 0 and ks["seconds"] > 0
+    gen = _run(pipe, B, n)
+    gen2 = _run(pipe, B, n)  # graph replay path when graphs=True
+    assert torch.equal(gen, gen2)
+    hid = _final_hidden(pipe, B).float()
+    ks = [pipe.kernel_stats(k) for k in range(4)]
     pipe.close()
+    assert all(k["launches"] > 0 and k["seconds"] > 0 for k in ks)
+    gen = gen.reshape(B, n).numpy()
+    prompt = synth.synth_tokens(B * s, synth.seed_for(3), VOCAB).reshape(B, s)
+    assert ((gen >= 0) & (gen < VOCAB)).all()
+    ck = _checkpoint(plan["layer_bits"])
+    seq = np.concatenate([prompt, gen[:, :n - 1]], axis=1)  # positions 0 .. s + n - 2
+    logits, x = _ref_logits_and_hidden(plan, ck, seq, cuda)
+    lg = logits[:, s - 1:].cpu()  # the logits that chose tokens 0 .. n-1
+    top = lg.max(dim=-1).values
+    picked = lg.gather(-1, torch.from_numpy(gen).long()[..., None])[..., 0]
+    # every generated token is the reference argmax up to a small logit margin
+    margin = float((top - picked).max())
+    assert margin < 0.05, margin
+    agree = float((lg.argmax(-1).numpy() == gen).mean())
+    assert agree >= 0.9, agree
+    ref = x[:, -1].cpu()
+    err = float((hid - ref).abs().max() / ref.abs().max())
+    assert err < 2e-2, err
 
 
 def test_graph_and_eager_bit_identical(cuda):
     import torch
     from paper_2403_01136_b200.pipeline import Pipeline
     plan, model_json = _plan(3)
-    outs = []
+    outs, hids = [], []
     for graphs in (True, False):
         pipe = Pipeline(json.dumps(plan), model_json, use_graphs=graphs)
-        o = torch.empty(8 * H1, dtype=torch.bfloat16).pin_memory()
-        pipe.run(None, o.data_ptr())
-        pipe.run(None, o.data_ptr())
-        outs.append(o.clone())
+        _run(pipe, 8, 3)
+        outs.append(_run(pipe, 8, 3))
+        hids.append(_final_hidden(pipe, 8))
         pipe.close()
-    assert torch.equal(outs[0], outs[1])
+    assert torch.equal(outs[0], outs[1]) and torch.equal(hids[0], hids[1])
 
 
-def test_host_prompt_path(cuda):
-    """e2e path: the prompt comes from pinned host memory."""
+def test_host_prompt_tokens_path(cuda):
+    """e2e path: the prompt token ids come from pinned host memory."""
     import torch
+
     from oracle import synth
     from paper_2403_01136_b200.pipeline import Pipeline
     plan, model_json = _plan(2)
     pipe = Pipeline(json.dumps(plan), model_json)
-    host_in = torch.from_numpy(synth.synth_bits(8 * 512 * H1, synth.seed_for(3), 0.0, 1.0)
-                               .view(np.int16)).view(torch.bfloat16).pin_memory()
-    a = torch.empty(8 * H1, dtype=torch.bfloat16).pin_memory()
-    b = torch.empty(8 * H1, dtype=torch.bfloat16).pin_memory()
-    pipe.run(None, a.data_ptr())
-    pipe.run(host_in.data_ptr(), b.data_ptr())
-    assert torch.equal(a, b)  # same bits whether the prompt was resident or uploaded
+    host = torch.from_numpy(synth.synth_tokens(8 * 512, synth.seed_for(3), VOCAB)).pin_memory()
+    a = _run(pipe, 8, 2)
+    b = _run(pipe, 8, 2, host)
+    assert torch.equal(a, b)  # same ids whether resident or uploaded
+    other = host.clone()
+    other[:512] = 7  # request 0 gets a different prompt
+    c = _run(pipe, 8, 2, other.pin_memory())
+    assert torch.equal(c.reshape(8, 2)[1:], a.reshape(8, 2)[1:])  # requests are independent
     pipe.close()
 
 
-def test_fused_decode_bit_identical_to_per_op(cuda):
-    """K3 fused decode units (decode_fused: one persistent launch per
-    bit-width run of the stage) produce the same bits as the default per-op
-    K3 launches; the mixed 4/8 plan makes the stage several runs."""
+def _weight_set(ck, plan, mode, tmp_path=None, bin_bytes=1 << 20):
+    """The synthetic checkpoint handed over explicitly: pageable numpy
+    buffers, pinned torch tensors, or one raw bf16 file with offsets."""
+    import torch
+    from paper_2403_01136_b200.pipeline import WeightSet
+    L = len(plan["layer_bits"])
+    w = WeightSet(L, bin_bytes=bin_bytes)
+    tensors = ([("linear", i, a) for i, a in enumerate(ck["linear"])] +
+               [("norm", i, a) for i, a in enumerate(ck["norm"])] +
+               [("embed", 0, ck["embed"]), ("pos", 0, ck["pos"]),
+                ("final_norm", 0, ck["lnf"][0]), ("final_norm", 1, ck["lnf"][1])])
+    if mode == "file":
+        path = tmp_path / "ckpt.bf16"
+        off = 0
+        with open(path, "wb") as f:
+            for kind, i, a in tensors:
+                buf = np.ascontiguousarray(a).tobytes()
+                f.write(buf)
+                _assign(w, kind, i, (path, off))
+                off += len(buf)
+        return w
+    for kind, i, a in tensors:
+        a = np.ascontiguousarray(a)
+        if mode == "pinned":
+            a = torch.from_numpy(a.view(np.int16)).pin_memory()
+        _assign(w, kind, i, a)
+    return w
+
+
+def _assign(w, kind, i, v):
+    if kind in ("linear", "norm"):
+        getattr(w, kind)[i] = v
+    elif kind == "final_norm":
+        w.final_norm[i] = v
+    else:
+        setattr(w, kind, v)
+
+
+@pytest.mark.parametrize("mode", ["pageable", "pinned", "file"])
+def test_weight_loader_bit_identical_to_synthetic(cuda, tmp_path, mode):
+    """The binned host/disk -> device loader with K1 per bin (1 MiB bins:
+    several 128-row blocks per op) serves exactly the weights the device
+    generator makes: generated tokens and final hidden states bit-identical."""
     import torch
     from paper_2403_01136_b200.pipeline import Pipeline
-    plan, model_json = _plan(5)
-    outs, launches = [], []
-    for fused in (True, False):
-        pipe = Pipeline(json.dumps(plan), model_json, decode_fused=fused, instrument=True)
-        o = torch.empty(8 * H1, dtype=torch.bfloat16).pin_memory()
-        pipe.run(None, o.data_ptr())
-        pipe.run(None, o.data_ptr())
-        outs.append(o.clone())
-        launches.append(pipe.info()["launches_per_round"])
-        pipe.close()
-    assert torch.equal(outs[0], outs[1])
-    assert launches[0] < launches[1]
+    plan, model_json = _plan(3)
+    base = Pipeline(json.dumps(plan), model_json)
+    ref_tok, ref_hid = _run(base, 8, 3), _final_hidden(base, 8)
+    base.close()
+    ck = _checkpoint(plan["layer_bits"])
+    ws = _weight_set(ck, plan, mode, tmp_path)
+    pipe = Pipeline(json.dumps(plan), model_json, weights=ws)
+    st = pipe.load_stats()
+    tok, hid = _run(pipe, 8, 3), _final_hidden(pipe, 8)
+    pipe.close()
+    assert torch.equal(tok, ref_tok) and torch.equal(hid, ref_hid)
+    src = sum(a.size for a in ck["linear"] + ck["norm"] + ck["lnf"]) * 2 + (ck["embed"].size + ck["pos"].size) * 2
+    assert st["source_bytes"] == src
+    assert st["bins"] > 4 * 12 and st["seconds"] > 0
+
+
+def test_weight_loader_rejects_bad_sources(cuda, tmp_path):
+    from paper_2403_01136_b200 import capi
+    from paper_2403_01136_b200.pipeline import Pipeline, WeightSet
+    plan, model_json = _plan(2)
+    w = WeightSet(12)
+    w.linear[0] = (tmp_path / "missing.bf16", 0)
+    with pytest.raises(capi.InvalidArgument):
+        Pipeline(json.dumps(plan), model_json, weights=w)
+    short = tmp_path / "short.bf16"
+    short.write_bytes(b"\0" * 1000)
+    w = WeightSet(12)
+    w.linear[1] = (short, 0)
+    with pytest.raises(capi.InvalidArgument):
+        Pipeline(json.dumps(plan), model_json, weights=w)

@@ -1,7 +1,9 @@
 """Multi-GPU pipeline parity (needs >= 2 GPUs; run with `gpurun --gpus 2`):
 a 2- (4-) stage OPT-125M-shaped plan executed over 2 processes / 2 B200s with
-NCCL P2P must produce final hidden states bit-identical to the same plan
-run as one stage on one GPU (same kernels, same order per layer)."""
+NCCL P2P (hidden states forward, next-token ids fed back from the last
+stage to stage 0) must produce generated tokens and final hidden states
+bit-identical to the same plan run as one stage on one GPU (same kernels,
+same order per layer)."""
 import json
 import os
 import socket
@@ -31,11 +33,13 @@ plan["stages"] = [{"device_index": j, "device": "b200", "layers": [cut[j], cut[j
 obj = [nccl_ids(world) if rank == 0 else None]
 dist.broadcast_object_list(obj, src=0)
 p = Pipeline(json.dumps(plan), model, rank, world, obj[0], sm_budget=140, timeout_s=60)
-out = torch.empty(8 * 768, dtype=torch.bfloat16).pin_memory()
+out = torch.empty(8 * 6, dtype=torch.int32).pin_memory()
 for _ in range(2):
     p.run(None, out.data_ptr() if rank == world - 1 else None)
 if rank == world - 1:
-    torch.save(out.clone(), os.environ["HP_OUT"])
+    hid = torch.empty(8 * 768, dtype=torch.bfloat16)
+    p.final_hidden(hid.data_ptr())
+    torch.save((out.clone(), hid), os.environ["HP_OUT"])
 p.close()
 dist.barrier()
 '''
@@ -59,9 +63,11 @@ def test_multistage_pipeline_bit_identical_to_single_gpu(cuda, tmp_path, world):
     one["device_order"] = [0]
     one["stages"] = [{"device_index": 0, "device": "b200", "layers": [0, 12]}]
     p = Pipeline(json.dumps(one), model, sm_budget=140, timeout_s=60)
-    ref = torch.empty(8 * 768, dtype=torch.bfloat16).pin_memory()
+    ref = torch.empty(8 * 6, dtype=torch.int32).pin_memory()
     for _ in range(2):
         p.run(None, ref.data_ptr())
+    ref_hid = torch.empty(8 * 768, dtype=torch.bfloat16)
+    p.final_hidden(ref_hid.data_ptr())
     p.close()
     w = tmp_path / "w.py"
     w.write_text(WORKER)
@@ -72,6 +78,7 @@ def test_multistage_pipeline_bit_identical_to_single_gpu(cuda, tmp_path, world):
                         f"--master-port={_port()}", str(w)], env=env, capture_output=True,
                        text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-4000:]
-    got = torch.load(outp)
-    assert torch.isfinite(got.float()).all()
+    got, hid = torch.load(outp)
+    assert torch.isfinite(hid.float()).all()
     assert torch.equal(got, ref)
+    assert torch.equal(hid, ref_hid)
