@@ -245,6 +245,18 @@ hp_status hp_pipeline_layer_costs(hp_pipeline* p, int phase, double* out, int64_
 hp_status hp_pipeline_info(hp_pipeline* p, int64_t* out4);
 void hp_pipeline_destroy(hp_pipeline* p);
 
+/* ---- micro-batch manager (hetplan::runtime::
+ * microbatch_manager): thread-safe status table of one round. prefill_done
+ * returns the group it made ready (its first decode token enqueued) or -1;
+ * decode_done enqueues the group's next token (*finished = 1 after token
+ * n-1); next pops the FIFO of ready decode items (returns 1, or 0 if empty). */
+typedef struct hp_mbm hp_mbm;
+hp_status hp_mbm_create(int B, int eta, int xi, int n, hp_mbm** out);
+hp_status hp_mbm_prefill_done(hp_mbm* m, int k, int* ready_group);
+hp_status hp_mbm_decode_done(hp_mbm* m, int group, int token, int* finished);
+int hp_mbm_next(hp_mbm* m, int* group, int* token);
+void hp_mbm_destroy(hp_mbm* m);
+
 /* ---- host planning helpers (drop-in hetplan:: library, plain types) -----
  * model9 = {num_layers, h1, h2, num_heads, vocab_s, pos_s, d_t, d_p,
  * norm(0 standard, 1 rms)}. Text outputs are NUL-terminated into out/cap.  */

@@ -123,6 +123,11 @@ def _load() -> C.CDLL:
         "hp_pipeline_layer_costs": (i32, [v, i32, P(d), i64, P(i64)]),
         "hp_pipeline_info": (i32, [v, P(i64)]),
         "hp_pipeline_destroy": (None, [v]),
+        "hp_mbm_create": (i32, [i32, i32, i32, i32, P(v)]),
+        "hp_mbm_prefill_done": (i32, [v, i32, P(i32)]),
+        "hp_mbm_decode_done": (i32, [v, i32, i32, P(i32)]),
+        "hp_mbm_next": (i32, [v, P(i32), P(i32)]),
+        "hp_mbm_destroy": (None, [v]),
         "hp_layernorm": (i32, [v, i64, i64, i64, v, v, v, i64, v]),
         "hp_embed": (i32, [v, i32, i32, i32, i32, v, v, i64, i64, i64, v, v]),
         "hp_attention_prefill": (i32, [v, i32, i32, i64, i32, v, v, v, i32, i32, v]),
@@ -152,7 +157,8 @@ EXPORTED = [
     "hp_nccl_unique_id", "hp_pipeline_create", "hp_pipeline_run", "hp_pipeline_stage_costs",
     "hp_pipeline_kernel_stats", "hp_pipeline_layer_costs", "hp_pipeline_info", "hp_pipeline_destroy",
     "hp_layernorm", "hp_embed", "hp_attention_prefill", "hp_attention_decode", "hp_argmax",
-    "hp_pipeline_final_hidden", "hp_pipeline_load_stats",
+    "hp_pipeline_final_hidden", "hp_pipeline_load_stats", "hp_mbm_create", "hp_mbm_prefill_done",
+    "hp_mbm_decode_done", "hp_mbm_next", "hp_mbm_destroy",
 ]
 
 

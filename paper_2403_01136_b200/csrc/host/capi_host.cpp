@@ -15,6 +15,7 @@
 #include "hetplan/pipesim/pipesim.hpp"
 #include "hetplan/plan/plan_io.hpp"
 #include "hetplan/runtime/pipeline.hpp"
+#include "hetplan/runtime/microbatch.hpp"
 #include <nccl.h>
 #include <json.hpp>
 #include "hetplan/types.hpp"
@@ -454,5 +455,57 @@ hp_status hp_pipeline_info(hp_pipeline* p, int64_t* out4) {
 }
 
 void hp_pipeline_destroy(hp_pipeline* p) { delete p; }
+
+struct hp_mbm {
+    std::unique_ptr<hetplan::runtime::microbatch_manager> m;
+};
+
+hp_status hp_mbm_create(int B, int eta, int xi, int n, hp_mbm** out) {
+    try {
+        if (!out) throw std::invalid_argument("mbm_create: NULL out");
+        auto h = std::make_unique<hp_mbm>();
+        h->m = std::make_unique<hetplan::runtime::microbatch_manager>(B, eta, xi, n);
+        *out = h.release();
+        return HP_OK;
+    } catch (const std::exception& e) {
+        return from_exception(e);
+    }
+}
+
+hp_status hp_mbm_prefill_done(hp_mbm* m, int k, int* ready_group) {
+    try {
+        if (!m) throw std::invalid_argument("mbm: NULL handle");
+        const int g = m->m->prefill_done(k);
+        if (ready_group) *ready_group = g;
+        return HP_OK;
+    } catch (const std::exception& e) {
+        return from_exception(e);
+    }
+}
+
+hp_status hp_mbm_decode_done(hp_mbm* m, int group, int token, int* finished) {
+    try {
+        if (!m) throw std::invalid_argument("mbm: NULL handle");
+        const bool f = m->m->decode_done(group, token);
+        if (finished) *finished = f ? 1 : 0;
+        return HP_OK;
+    } catch (const std::logic_error& e) {
+        hp_detail::set_error(e.what());
+        return HP_EINVAL;
+    } catch (const std::exception& e) {
+        return from_exception(e);
+    }
+}
+
+int hp_mbm_next(hp_mbm* m, int* group, int* token) {
+    if (!m || !group || !token) return 0;
+    hetplan::runtime::microbatch_manager::decode_item it{};
+    if (!m->m->next_decode(it)) return 0;
+    *group = it.group;
+    *token = it.token;
+    return 1;
+}
+
+void hp_mbm_destroy(hp_mbm* m) { delete m; }
 
 }  // extern "C"

@@ -14,6 +14,7 @@
 //     graph per rank after an eager warm-up round;
 //   * weights are loaded once, through the binned H2D + K1 loader below.
 #include "hetplan/runtime/pipeline.hpp"
+#include "hetplan/runtime/microbatch.hpp"
 
 #include <cuda_runtime.h>
 #include <nccl.h>
@@ -623,18 +624,20 @@ struct pipeline::impl {
         cuda_ok(cudaStreamSynchronize(cs), "init");
     }
 
-    // feedback messages last -> 0 (token ids), in the last stage's emission order
+    // feedback messages last -> 0 (token ids), in the last stage's emission
+    // order: the micro-batch manager replays the last stage's completions
+    // (a group's first tokens go out when its last prefill batch is done)
     std::vector<unit_ref> feedback_order() const {
         std::vector<unit_ref> out;
         if (world == 1) return out;
-        std::vector<int> left(sched.num_groups, 0);
-        for (int g : sched.group_of_prefill) ++left[g];
+        microbatch_manager m(B, eta, xi, n);
         for (const unit_ref& u : last_units) {
             if (u.kind == pipesim::unit_kind::prefill) {
-                const int g = sched.group_of_prefill[u.index];
-                if (--left[g] == 0 && n >= 2) out.push_back({pipesim::unit_kind::decode, g, 1});
-            } else if (u.token + 1 <= n - 1) {
-                out.push_back({pipesim::unit_kind::decode, u.index, u.token + 1});
+                const int g = m.prefill_done(u.index);
+                if (g >= 0 && n >= 2) out.push_back({pipesim::unit_kind::decode, g, 1});
+            } else {
+                m.decode_done(u.index, u.token);
+                if (u.token + 1 <= n - 1) out.push_back({pipesim::unit_kind::decode, u.index, u.token + 1});
             }
         }
         return out;
@@ -853,8 +856,7 @@ struct pipeline::impl {
                 recv_idx[{static_cast<int>(u.kind), u.index, u.token}] = static_cast<int>(i);
             }
         }
-        std::vector<int> left(sched.num_groups, 0);
-        for (int g : sched.group_of_prefill) ++left[g];
+        microbatch_manager mbm(B, eta, xi, n);  // the round's status table
         int comp_i = 0;
 
         for (size_t ui = 0; ui < units.size(); ++ui) {
@@ -891,14 +893,15 @@ struct pipeline::impl {
                 send_after_compute(x, static_cast<size_t>(m) * h1, ncclBfloat16, comp_i);
                 continue;
             }
+            // a prefill batch may straddle a group boundary: the group's
+            // tokens are complete once the manager marks its last batch done
+            const int ready = pre ? mbm.prefill_done(u.index) : -1;
+            if (!pre) mbm.decode_done(u.index, u.token);
             if (world == 1) continue;
             if (pre) {
-                const int g = sched.group_of_prefill[u.index];
-                // a prefill batch may straddle a group boundary: its tokens
-                // are complete once the group's last batch is done
-                if (--left[g] == 0 && n >= 2)
-                    send_after_compute(cur_tok + group_first[g], static_cast<size_t>(group_size[g]), ncclInt32,
-                                       comp_i);
+                if (ready >= 0 && n >= 2)
+                    send_after_compute(cur_tok + group_first[ready], static_cast<size_t>(group_size[ready]),
+                                       ncclInt32, comp_i);
             } else if (u.token + 1 <= n - 1) {
                 send_after_compute(cur_tok + group_first[u.index], static_cast<size_t>(group_size[u.index]),
                                    ncclInt32, comp_i);

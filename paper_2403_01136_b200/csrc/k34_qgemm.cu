@@ -752,8 +752,13 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
                         float f[16];
 #pragma unroll
                         for (int i = 0; i < 16; ++i) f[i] = 0.f;
+#ifdef HP_EXP_NORED  // timing experiment: the straggler skips the partial reads
+                        const int nred = 0;
+#else
+                        const int nred = sg.nseg;
+#endif
 #pragma unroll 1
-                        for (int jb = 0; jb < sg.nseg; jb += kRB) {
+                        for (int jb = 0; jb < nred; jb += kRB) {
                             float4 q4[kRB][4];
 #pragma unroll
                             for (int jj = 0; jj < kRB; ++jj) {
@@ -924,6 +929,7 @@ qgemm_plan plan_qgemm(int64_t n_out, int64_t k_in, int64_t m, int phase) {
                          tiles <= static_cast<int64_t>(kTicketBytes / 4)
                      ? 1
                      : 0;
+    if (phase == 1 && getenv("HP_EXP_DECODE_TILES")) p.stream_k = 0;  // timing experiment
     p.dp = 0;
     if (p.stream_k && prefill_sk) {
         // optional data-parallel + stream-K split: whole-tile waves first,
