@@ -47,6 +47,13 @@ CONFIGS = {
     # 44 GiB budget (KV alone is 26.9 GB at B = 32) makes the plan mixed
     "opt30b_b32_1gpu": dict(model="opt-30b", devices=1, mem=44 * GiB, B=32, supported=None,
                             group=1, omega="survey"),
+    # SURVEY §8f rank 1, the LLM-PQ loop closed on B200: the same configs
+    # planned with the latency model FITTED on this build's kernels
+    # (tools/latency_profile.py -> b200_<model>.latency_model.json)
+    "opt13b_b32_1gpu_b200lat": dict(model="opt-13b", devices=1, mem=22 * GiB, B=32, supported=None,
+                                    group=1, omega="survey", latency="b200_opt13b"),
+    "opt30b_b32_1gpu_b200lat": dict(model="opt-30b", devices=1, mem=44 * GiB, B=32, supported=None,
+                                    group=1, omega="survey", latency="b200_opt30b"),
     "opt30b_b32_2gpu": dict(model="opt-30b", devices=2, mem=24 * GiB, B=32, supported=None,
                             group=2, omega="survey"),
     "opt30b_b32_4gpu": dict(model="opt-30b", devices=4, mem=12 * GiB, B=32, supported=None,
@@ -67,6 +74,17 @@ def latency_json(model: str) -> str:
         per_bit[str(b)] = {"prefill": [5e-6, 0.0, 0.0, 2 * P / (FL * eff), 4 * h1 / FL],
                            "decode": [5e-6 + P * b / 8 / BW, 0.0, 4 * h1 / BW, 0.0]}
     return json.dumps({"b200": per_bit})
+
+
+def measured_latency_json(stem: str) -> str:
+    """The fitted B200 model (latcost serialize_model format, from
+    tools/latency_profile.py) in the planner input schema
+    {device: {bit: {"prefill": [5], "decode": [4]}}}."""
+    m = json.loads((OUT / f"{stem}.latency_model.json").read_text())
+    out: dict = {}
+    for g in m["groups"]:
+        out.setdefault(g["device"], {}).setdefault(str(g["bit"]), {})[g["phase"]] = g["coeffs"]
+    return json.dumps(out)
 
 
 def omega_survey(L: int) -> str:
@@ -106,6 +124,7 @@ def run(name: str) -> str:
     c = CONFIGS[name]
     L = SHAPES[c["model"]][0]
     omega = omega_from_synthetic(c["model"]) if c["omega"] == "synthetic-weights" else omega_survey(L)
+    lat = (measured_latency_json(c["latency"]) if c.get("latency") else latency_json(c["model"]))
     dev = {"name": "b200", "mem_bytes": c["mem"], "link_bw_bytes_per_s": 9e11}
     if c["supported"]:
         dev["supported_bits"] = c["supported"]
@@ -113,7 +132,7 @@ def run(name: str) -> str:
            "cluster": {"devices": [dev] * c["devices"]},
            "workload": {"B": c["B"], "s": 512, "n": 100}, "bits": [3, 4, 8, 16]}
     t0 = time.time()
-    plan = oracle.ref().best_plan(json.dumps(cfg), omega, latency_json(c["model"]), 0.001,
+    plan = oracle.ref().best_plan(json.dumps(cfg), omega, lat, 0.001,
                                   group=c["group"], heuristic=False, time_limit_s=5.0)
     dt = time.time() - t0
     doc = json.loads(plan)
@@ -122,7 +141,7 @@ def run(name: str) -> str:
     (OUT / f"{name}.json").write_text(json.dumps(doc, indent=1))
     (OUT / f"{name}.omega.csv").write_text(omega)
     (OUT / f"{name}.config.json").write_text(json.dumps(cfg, indent=1))
-    (OUT / f"{name}.latency.json").write_text(latency_json(c["model"]))
+    (OUT / f"{name}.latency.json").write_text(lat)
     return f"{name}: {dt:.0f}s bits={doc['layer_bits']} stages={[s['layers'] for s in doc['stages']]} eta={doc['eta']} xi={doc['xi']} optimal={doc['optimal']}"
 
 
