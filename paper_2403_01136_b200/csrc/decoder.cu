@@ -10,7 +10,7 @@
 //     layer);
 //   * attn_decode_kernel: one query per request against its cache rows
 //     [0, p] after appending the new K/V row at position p (HBM-bound: the
-//     K/V stream dominates, 128-bit coalesced loads, 8 keys in flight per
+//     K/V stream dominates, coalesced 256 B rows, 16 keys in flight per
 //     warp, fp32 online softmax);
 //   * argmax_kernel: greedy next token of every LM-head row (ties -> lowest
 //     id).
@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(128)
                        __nv_bfloat16* __restrict__ out, __nv_bfloat16* __restrict__ kc,
                        __nv_bfloat16* __restrict__ vc, int req0, int S_max) {
     constexpr int EL = D / 32;  // dims per lane (2 or 4)
-    constexpr int KU = 8;       // keys in flight per warp
+    constexpr int KU = 16;      // keys in flight per warp (8 measured 0.71 of HBM)
     __shared__ float s_sc[1024 + 32];
     __shared__ float s_red[4][D + 2];
     pdl_wait_glue();
