@@ -57,6 +57,9 @@
 #ifndef HP_CR_CAP
 #define HP_CR_CAP 12
 #endif
+#ifndef HP_DEC_CORES
+#define HP_DEC_CORES 0
+#endif
 
 // The MMA issuer is one latency-critical warp: it spins on its barriers
 // instead of suspending (40-layer decode step -0.7%; HP_MMA_SPIN=0 restores
@@ -206,11 +209,15 @@ struct qgemm_cfg {
     // stages round-robin (amortises the per-stage barrier work over 8
     // slices per warp); prefill and 16-bit decode use 2 warpgroups splitting
     // every stage. One CTA per SM (all 512 TMEM columns).
-    static constexpr bool kCoRes = false;
-    static constexpr int kMinBlocks = 1;
-    static constexpr int kTmemCols = 512;
+    // HP_DEC_CORES: decode CTAs sized to half an SM (256 TMEM columns,
+    // <= 110 KB smem, 4 warpgroups at <= 64 registers) so TWO co-reside:
+    // the grid is 2 x SMs, and a CTA of the next op (PDL) takes the slot of
+    // a finished one while the rest of the current op drains.
+    static constexpr bool kCoRes = BN <= 64 && HP_DEC_CORES;
+    static constexpr int kMinBlocks = kCoRes ? 2 : 1;
+    static constexpr int kTmemCols = kCoRes ? 256 : 512;
     static constexpr bool kRR = BN <= 64 && BITS != 16;
-    static constexpr int DWG = kRR ? HP_DWG : 2;
+    static constexpr int DWG = kRR ? (kCoRes ? 2 : HP_DWG) : 2;
     static constexpr int kThreads = 128 * (2 + DWG);
     static constexpr int kEpiWarp0 = 4 + 4 * DWG;
     static constexpr int NG = SPS >= 4 ? SPS / 4 : 1;            // groups touched per stage
@@ -225,8 +232,8 @@ struct qgemm_cfg {
 #ifndef HP_PRE_BUDGET_KB
 #define HP_PRE_BUDGET_KB 186
 #endif
-    static constexpr int kBudget = (BN <= 64 ? HP_DEC_BUDGET_KB : HP_PRE_BUDGET_KB) * 1024;
-    static constexpr int BR = BN <= 64 ? HP_DEC_BR : (BN <= 128 ? 6 : 4);
+    static constexpr int kBudget = (kCoRes ? 100 : (BN <= 64 ? HP_DEC_BUDGET_KB : HP_PRE_BUDGET_KB)) * 1024;
+    static constexpr int BR = kCoRes ? 4 : (BN <= 64 ? HP_DEC_BR : (BN <= 128 ? 6 : 4));
     static constexpr int CR_ = (kBudget - BR * kB) / kCS > HP_CR_CAP ? HP_CR_CAP : (kBudget - BR * kB) / kCS;
     // Round-robin consumers wait only on their own stages, so every ring slot
     // they consume must always belong to the same warpgroup (depth % DWG ==
@@ -826,9 +833,9 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
 // amortise the per-stage barrier/issue work; prefill moves half a group so
 // the [BN x 64] activation tile per stage is small and the pipeline deep.
 template <int BITS, int BN>
-constexpr int kSlicesPerStage = BN <= 64 ? (BITS >= 8 ? 4 : HP_DEC_SPS) : 2;
+constexpr int kSlicesPerStage = BN <= 64 ? (BITS >= 8 || HP_DEC_CORES ? 4 : HP_DEC_SPS) : 2;
 
-int slices_per_stage(int bits, int bn) { return bn <= 64 ? (bits >= 8 ? 4 : HP_DEC_SPS) : 2; }
+int slices_per_stage(int bits, int bn) { return bn <= 64 ? (bits >= 8 || HP_DEC_CORES ? 4 : HP_DEC_SPS) : 2; }
 
 namespace {
 
@@ -903,7 +910,8 @@ qgemm_plan plan_qgemm(int64_t n_out, int64_t k_in, int64_t m, int phase) {
     qgemm_plan p{};
     const int G = static_cast<int>(ceil_div64(k_in, 128));
     const int NT = static_cast<int>(ceil_div64(n_out, 128));
-    const int sms = num_sms();
+    // co-resident decode CTAs (HP_DEC_CORES): two per SM
+    const int sms = num_sms() * ((phase == 1 && m <= 32 && HP_DEC_CORES) ? 2 : 1);
     if (phase == 1 && m <= 32) {
         p.bn = m <= 16 ? 16 : 32;
     } else {

@@ -27,11 +27,17 @@ H1, H2, HEADS, VOCAB, POS = 768, 3072, 12, 50272, 2050
 SHAPES = [(3 * H1, H1), (H1, H1), (H2, H1), (H1, H2)]
 
 
-def _plan(n=4):
+def _plan(n=4, eta=None):
     from paper_2403_01136_b200.pipeline import load_plan
     plan_json, model_json = load_plan("opt125m_b8_1gpu")
     plan = json.loads(plan_json)
     plan["workload"]["n"] = n  # xi == B: the objective does not depend on n
+    if eta is not None:  # re-batch the prefill; recompose Eq. (4) (types.cpp:17-24)
+        plan["eta"] = eta
+        o, B = plan["objective"], plan["workload"]["global_bz"]
+        bc = lambda u: -(-(B - u) // u)
+        o["total"] = (bc(eta) * o["t_max_pre"] + bc(plan["xi"]) * (n - 1) * o["t_max_dec"]
+                      + o["t_pre_total"] + o["t_dec_total"] + o["theta"] * o["omega_sum"])
     return plan, model_json
 
 
@@ -121,14 +127,16 @@ def _final_hidden(pipe, B):
     return h.reshape(B, H1)
 
 
-@pytest.mark.parametrize("graphs", [True, False])
-def test_opt125m_round_matches_reference_decoder(cuda, graphs):
+@pytest.mark.parametrize("graphs,eta", [(True, None), (False, None), (True, 3)])
+def test_opt125m_round_matches_reference_decoder(cuda, graphs, eta):
+    """eta = 3 with B = 8: a ragged last prefill micro-batch (3, 3, 2), the
+    case whose stream-K workspace was once undersized."""
     import torch
 
     from oracle import synth
     from paper_2403_01136_b200.pipeline import Pipeline
     n = 4
-    plan, model_json = _plan(n)
+    plan, model_json = _plan(n, eta)
     B, s = 8, 512
     pipe = Pipeline(json.dumps(plan), model_json, use_graphs=graphs, instrument=True)
     gen = _run(pipe, B, n)
