@@ -9,9 +9,9 @@
 //     pre-allocated KV cache (memcost.cpp:38-42: 2*v*(s+n)*h1 elements per
 //     layer);
 //   * attn_decode_kernel: one query per request against its cache rows
-//     [0, p] after appending the new K/V row at position p (HBM-bound: the
-//     K/V stream dominates, coalesced 256 B rows, 16 keys in flight per
-//     warp, fp32 online softmax);
+//     [0, p] after appending the new K/V row at position p (HBM-bound: one
+//     streaming pass over K and V, coalesced 256 B rows, flash-decoding
+//     online softmax in fp32);
 //   * argmax_kernel: greedy next token of every LM-head row (ties -> lowest
 //     id).
 // qkv rows are [q (h1) | k (h1) | v (h1)], head h at columns h*D .. h*D+D-1
@@ -20,6 +20,7 @@
 
 #include <cfloat>
 #include <cstdint>
+#include <type_traits>
 
 namespace hp {
 
@@ -124,16 +125,17 @@ __device__ __forceinline__ uint32_t tile_off(int row, int chunk) {
 }
 
 // ---------------------------------------------------------- prefill attention
-// grid (q-tiles of 64, heads, requests); 4 warps x 16 query rows.
+// grid (q-tiles of 16*NW, heads, requests); NW warps x 16 query rows.
 // qkv [rows x 3h] bf16 (request r's tokens at rows r*s .. r*s+s-1 of this
 // micro-batch); out [rows x h]; K/V cache rows of request (req0 + r) at
 // positions 0..s-1: cache + ((req0+r)*S_max + pos)*h.
-template <int D>
-__global__ void __launch_bounds__(128)
+template <int D, int NW>
+__global__ void __launch_bounds__(32 * NW)
     attn_prefill_kernel(const __nv_bfloat16* __restrict__ qkv, int s, int h, float scale_log2,
                         __nv_bfloat16* __restrict__ out, __nv_bfloat16* __restrict__ kc,
                         __nv_bfloat16* __restrict__ vc, int req0, int S_max) {
-    constexpr int BR = 64, BC = 64, CH = D / 8;  // 16-byte chunks per row
+    constexpr int BR = 16 * NW, BC = 64, CH = D / 8;  // 16-byte chunks per row
+    constexpr int NT = 32 * NW;
     extern __shared__ __align__(128) uint8_t sm[];
     uint8_t* sQ = sm;
     uint8_t* sK = sm + BR * D * 2;          // 2 stages
@@ -147,7 +149,7 @@ __global__ void __launch_bounds__(128)
     const int q0 = qt * BR;
     // Q tile + KV cache rows of this q-tile (each K/V row is written once:
     // by the CTA whose query tile covers it)
-    for (int i = tid; i < BR * CH; i += 128) {
+    for (int i = tid; i < BR * CH; i += NT) {
         const int row = i / CH, c = i % CH;
         const bool ok = q0 + row < s;
         cp_async16(smem_addr(sQ) + tile_off<D>(row, c), base + static_cast<int64_t>(q0 + row) * ld + c * 8,
@@ -163,7 +165,7 @@ __global__ void __launch_bounds__(128)
     cp_commit();
     const int nkv = (q0 + BR + BC - 1) / BC;  // causal: key tiles 0 .. q-tile
     auto load_kv = [&](int j, int stg) {
-        for (int i = tid; i < BC * CH; i += 128) {
+        for (int i = tid; i < BC * CH; i += NT) {
             const int row = i / CH, c = i % CH;
             const int key = j * BC + row;
             const bool ok = key < s;
@@ -297,16 +299,23 @@ __global__ void __launch_bounds__(128)
 
 // ----------------------------------------------------------- decode attention
 // grid (heads, rows); 4 warps. Row r (request req0 + r): query q = qkv[r, head],
-// appends k/v at position p, attends over cache rows 0..p.
+// appends k/v at position p, attends over cache rows 0..p in ONE streaming
+// pass: warp w takes keys w*KU.. in chunks of KU, issues the chunk's K and V
+// row loads together (lanes split the head dim: 256 B per row per warp),
+// and keeps a flash-decoding online softmax (running max m, sum l, and the
+// rescaled fp32 accumulator); the 4 warps' (m, l, acc) merge in shared
+// memory. (The two-pass version -- all K rows, a block-wide softmax, then
+// all V rows -- ran at 0.71 of HBM: each pass drained before the next.)
 template <int D>
 __global__ void __launch_bounds__(128)
     attn_decode_kernel(const __nv_bfloat16* __restrict__ qkv, int h, int p, float scale_log2,
                        __nv_bfloat16* __restrict__ out, __nv_bfloat16* __restrict__ kc,
                        __nv_bfloat16* __restrict__ vc, int req0, int S_max) {
     constexpr int EL = D / 32;  // dims per lane (2 or 4)
-    constexpr int KU = 16;      // keys in flight per warp (8 measured 0.71 of HBM)
-    __shared__ float s_sc[1024 + 32];
-    __shared__ float s_red[4][D + 2];
+    constexpr int KU = 8;       // keys per chunk: 2*KU row loads in flight per lane
+    using raw_t = typename std::conditional<EL == 4, uint2, uint32_t>::type;
+    __shared__ float s_m[4], s_l[4];
+    __shared__ float s_acc[4][D];
     pdl_wait_glue();
     pdl_trigger_glue();
     const int head = blockIdx.x, r = blockIdx.y;
@@ -314,106 +323,89 @@ __global__ void __launch_bounds__(128)
     const int64_t ld = 3LL * h;
     const __nv_bfloat16* row = qkv + static_cast<int64_t>(r) * ld + head * D;
     const int64_t cbase = static_cast<int64_t>(req0 + r) * S_max * h + head * D;
-    // append k/v at p (one warp), q into registers (every warp)
     float q[EL];
-    {
-        const __nv_bfloat16* qp = row + lane * EL;
 #pragma unroll
-        for (int e = 0; e < EL; ++e) q[e] = __bfloat162float(qp[e]) * scale_log2;
-        if (warp == 0) {
+    for (int e = 0; e < EL; ++e) q[e] = __bfloat162float(row[lane * EL + e]) * scale_log2;
+    if (warp == 0) {  // append k/v at p
 #pragma unroll
-            for (int e = 0; e < EL; ++e) {
-                kc[cbase + static_cast<int64_t>(p) * h + lane * EL + e] = row[h + lane * EL + e];
-                vc[cbase + static_cast<int64_t>(p) * h + lane * EL + e] = row[2 * h + lane * EL + e];
-            }
+        for (int e = 0; e < EL; ++e) {
+            kc[cbase + static_cast<int64_t>(p) * h + lane * EL + e] = row[h + lane * EL + e];
+            vc[cbase + static_cast<int64_t>(p) * h + lane * EL + e] = row[2 * h + lane * EL + e];
         }
     }
     __syncthreads();  // the new row is visible to the CTA (same-CTA global RAW)
     const int nk = p + 1;
-    auto loadv = [&](const __nv_bfloat16* src, float* f) {
+    auto unpack = [&](raw_t v, float* f) {
         if constexpr (EL == 4) {
-            const uint2 u = *reinterpret_cast<const uint2*>(src);
-            const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
-            const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+            const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.x));
+            const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.y));
             f[0] = a.x; f[1] = a.y; f[2] = b.x; f[3] = b.y;
         } else {
-            const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(src));
+            const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v));
             f[0] = a.x; f[1] = a.y;
         }
     };
-    // scores (log2 domain): warp w takes keys w, w+4, ... KU at a time
-    float wmax = -FLT_MAX;
+    float m = -FLT_MAX, l = 0.f, acc[EL];
+#pragma unroll
+    for (int e = 0; e < EL; ++e) acc[e] = 0.f;
     for (int k0 = warp * KU; k0 < nk; k0 += 4 * KU) {
-        float part[KU];
+        raw_t kr[KU], vr[KU];
 #pragma unroll
         for (int u = 0; u < KU; ++u) {
-            const int key = k0 + u;
-            float f[EL];
-            if (key < nk) {
-                loadv(kc + cbase + static_cast<int64_t>(key) * h + lane * EL, f);
-            } else {
+            const int key = k0 + u < nk ? k0 + u : nk - 1;  // clamp: loads stay in bounds
+            kr[u] = *reinterpret_cast<const raw_t*>(kc + cbase + static_cast<int64_t>(key) * h + lane * EL);
+            vr[u] = *reinterpret_cast<const raw_t*>(vc + cbase + static_cast<int64_t>(key) * h + lane * EL);
+        }
+        float sc[KU];
 #pragma unroll
-                for (int e = 0; e < EL; ++e) f[e] = 0.f;
-            }
+        for (int u = 0; u < KU; ++u) {
+            float f[EL];
+            unpack(kr[u], f);
             float a = 0.f;
 #pragma unroll
             for (int e = 0; e < EL; ++e) a = fmaf(q[e], f[e], a);
-            part[u] = a;
+            sc[u] = a;
         }
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1)
 #pragma unroll
-            for (int u = 0; u < KU; ++u) part[u] += __shfl_xor_sync(0xffffffffu, part[u], d);
-        if (lane < KU && k0 + lane < nk) {
-            float v = part[0];
-#pragma unroll
-            for (int u = 1; u < KU; ++u) v = lane == u ? part[u] : v;
-            s_sc[k0 + lane] = v;
-        }
+            for (int u = 0; u < KU; ++u) sc[u] += __shfl_xor_sync(0xffffffffu, sc[u], d);
+        float cm = m;
 #pragma unroll
         for (int u = 0; u < KU; ++u)
-            if (k0 + u < nk) wmax = fmaxf(wmax, part[u]);
-    }
-    if (lane == 0) s_red[warp][0] = wmax;
-    __syncthreads();
-    const float m = fmaxf(fmaxf(s_red[0][0], s_red[1][0]), fmaxf(s_red[2][0], s_red[3][0]));
-    __syncthreads();
-    // probabilities + row sum
-    float psum = 0.f;
-    for (int k = tid; k < nk; k += 128) {
-        const float e = exp2f(s_sc[k] - m);
-        s_sc[k] = e;
-        psum += e;
-    }
+            if (k0 + u < nk) cm = fmaxf(cm, sc[u]);
+        const float corr = exp2f(m - cm);
+        l *= corr;
 #pragma unroll
-    for (int d = 16; d > 0; d >>= 1) psum += __shfl_xor_sync(0xffffffffu, psum, d);
-    if (lane == 0) s_red[warp][1] = psum;
-    __syncthreads();
-    const float l = s_red[0][1] + s_red[1][1] + s_red[2][1] + s_red[3][1];
-    __syncthreads();
-    // O = sum_k p_k V_k: warp w takes keys w*KU.., lanes split the dims
-    float acc[EL];
-#pragma unroll
-    for (int e = 0; e < EL; ++e) acc[e] = 0.f;
-    for (int k0 = warp * KU; k0 < nk; k0 += 4 * KU) {
+        for (int e = 0; e < EL; ++e) acc[e] *= corr;
 #pragma unroll
         for (int u = 0; u < KU; ++u) {
-            const int key = k0 + u;
-            if (key < nk) {
-                float f[EL];
-                loadv(vc + cbase + static_cast<int64_t>(key) * h + lane * EL, f);
-                const float pk = s_sc[key];
+            const float pk = k0 + u < nk ? exp2f(sc[u] - cm) : 0.f;
+            l += pk;
+            float f[EL];
+            unpack(vr[u], f);
 #pragma unroll
-                for (int e = 0; e < EL; ++e) acc[e] = fmaf(pk, f[e], acc[e]);
-            }
+            for (int e = 0; e < EL; ++e) acc[e] = fmaf(pk, f[e], acc[e]);
         }
+        m = cm;
+    }
+    if (lane == 0) {
+        s_m[warp] = m;
+        s_l[warp] = l;
     }
 #pragma unroll
-    for (int e = 0; e < EL; ++e) s_red[warp][lane * EL + e] = acc[e];
+    for (int e = 0; e < EL; ++e) s_acc[warp][lane * EL + e] = acc[e];
     __syncthreads();
     if (tid < D) {
-        const float v = (s_red[0][tid] + s_red[1][tid] + s_red[2][tid] + s_red[3][tid]) / l;
-        out[static_cast<int64_t>(r) * h + head * D + tid] = __float2bfloat16_rn(v);
+        const float M = fmaxf(fmaxf(s_m[0], s_m[1]), fmaxf(s_m[2], s_m[3]));
+        float L = 0.f, v = 0.f;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            const float c = s_m[w] == -FLT_MAX ? 0.f : exp2f(s_m[w] - M);  // empty warp: no keys
+            L += s_l[w] * c;
+            v += s_acc[w][tid] * c;
+        }
+        out[static_cast<int64_t>(r) * h + head * D + tid] = __float2bfloat16_rn(v / L);
     }
 }
 
@@ -476,7 +468,11 @@ __global__ void synth_tokens_kernel(int32_t* out, int64_t n, uint64_t seed, int6
 
 }  // namespace
 
-int attn_prefill_smem(int D) { return (64 * D * 2) * 5; }
+// 4 warps x 16 query rows: 80 KB at D = 128 (2 CTAs per SM); 8 warps
+// would not raise occupancy: at 186 registers one 256-thread CTA fills the
+// register file
+constexpr int kPrefillWarps = 4;
+int attn_prefill_smem(int D) { return (16 * kPrefillWarps * D * 2) + 4 * (64 * D * 2); }
 
 cudaError_t launch_embed(const int32_t* tok, int rows, int pos0, int pos_per_req, int s_tokens,
                          const void* E, const void* P, int pos_s, int h, int64_t vocab, void* x,
@@ -497,19 +493,19 @@ cudaError_t launch_attn_prefill(const void* qkv, int reqs, int s, int h, int D, 
     __nv_bfloat16* k = static_cast<__nv_bfloat16*>(kc);
     __nv_bfloat16* v = static_cast<__nv_bfloat16*>(vc);
     void* args[] = {&q, &s, &h, const_cast<float*>(&scale_log2), &o, &k, &v, &req0, &S_max};
-    const dim3 grid((s + 63) / 64, h / D, reqs);
+    const dim3 grid((s + 16 * kPrefillWarps - 1) / (16 * kPrefillWarps), h / D, reqs);
     const int smem = attn_prefill_smem(D);
     const void* fn;
     if (D == 128) {
-        fn = reinterpret_cast<const void*>(attn_prefill_kernel<128>);
+        fn = reinterpret_cast<const void*>(attn_prefill_kernel<128, kPrefillWarps>);
     } else if (D == 64) {
-        fn = reinterpret_cast<const void*>(attn_prefill_kernel<64>);
+        fn = reinterpret_cast<const void*>(attn_prefill_kernel<64, kPrefillWarps>);
     } else {
         return cudaErrorInvalidValue;
     }
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    return launch_ex(fn, grid, dim3(128), smem, st, args);
+    return launch_ex(fn, grid, dim3(32 * kPrefillWarps), smem, st, args);
 }
 
 cudaError_t launch_attn_decode(const void* qkv, int rows, int h, int D, int p, void* out, void* kc,

@@ -5,7 +5,7 @@
       `ncu --metrics gpu__time_duration.sum --clock-control none
        --profile-from-start off --csv --log-file launches.csv python bench.py ...`
       (bench.py brackets its timed rounds with cudaProfilerStart/Stop).
-  traffic <rep.ncu-rep> <k3|k4> <plan> [--out profiles/ncu_traffic.json]
+  traffic <rep.ncu-rep> <k3|k4> <plan> [--layer L] [--out profiles/ncu_traffic.json]
       DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of
       the first 4 matching qgemm launches of the timed round -- layer 0's
       qkv/out/fc1/fc2 of the first decode (k3) or prefill (k4) unit -- next
@@ -32,6 +32,8 @@ def kernel_class(name: str) -> str:
         bn = int(name.split("qgemm_kernel<")[1].split(",")[2])
         return "K3 decode qgemm (BN<=64)" if bn <= 64 else "K4 prefill qgemm (BN>=128)"
     for key, cls in (("layernorm", "layernorm (glue)"), ("gather_rows", "gather_rows (glue)"),
+                     ("attn_prefill", "attention prefill (glue)"), ("attn_decode", "attention decode (glue)"),
+                     ("embed_kernel", "embedding (glue)"), ("argmax", "argmax (glue)"),
                      ("nccl", "NCCL"), ("quant_pack", "K1 quant_pack"), ("stats_kernel", "K2 stats")):
         if key in name.lower():
             return cls
@@ -45,19 +47,24 @@ def rows_of(text: str):
 
 def round_counts(plan_name: str):
     """Launches per class in ONE full round of the plan on one stage (the
-    executor's forward: per layer 2 LN + 4 qgemm; 1 gather per prefill unit
-    that does not straddle a decode-group boundary)."""
+    executor's forward: per layer 2 LN + 4 qgemm + 1 attention; per unit an
+    embedding on stage 0 and gather + final LN + LM-head qgemm + argmax on the
+    last stage -- the LM head is a BN<=64 qgemm, counted with K3)."""
     plan = json.loads((PLANS / f"{plan_name}.json").read_text())
     B, n = plan["workload"]["global_bz"], plan["workload"]["n"]
     eta, xi = plan["eta"], plan["xi"]
     layers = len(plan["layer_bits"])
     pre_units = -(-B // eta)
     dec_units = -(-B // xi) * (n - 1)
+    units = pre_units + dec_units
     return {"K4 prefill qgemm (BN>=128)": 4 * layers * pre_units,
-            "K3 decode qgemm (BN<=64)": 4 * layers * dec_units,
-            "layernorm prefill (glue)": 2 * layers * pre_units,
-            "layernorm decode (glue)": 2 * layers * dec_units,
-            "gather_rows (glue)": pre_units}
+            "K3 decode qgemm (BN<=64)": 4 * layers * dec_units + units,
+            "layernorm prefill (glue)": 2 * layers * pre_units + pre_units,
+            "layernorm decode (glue)": 2 * layers * dec_units + dec_units,
+            "attention prefill (glue)": layers * pre_units,
+            "attention decode (glue)": layers * dec_units,
+            "embedding (glue)": units, "argmax (glue)": units,
+            "gather_rows (glue)": units}
 
 
 def launches(path: str, out: str, plan_name: str | None = None) -> None:
@@ -99,11 +106,11 @@ def launches(path: str, out: str, plan_name: str | None = None) -> None:
     print(json.dumps(res, indent=1))
 
 
-def alg_bytes(plan_name: str, kind: str):
+def alg_bytes(plan_name: str, kind: str, layer: int = 0):
     plan = json.loads((PLANS / f"{plan_name}.json").read_text())
     model = json.loads((PLANS / f"{plan_name}.config.json").read_text())["model"]
     h1, h2 = (model["h1"], model["h2"]) if "h1" in model else PRESET_H[model["preset"]]
-    bits = plan["layer_bits"][0]
+    bits = plan["layer_bits"][layer]
     scheme = 1
     if kind == "k3":
         m = min(plan["xi"], plan["workload"]["global_bz"])
@@ -118,11 +125,11 @@ def alg_bytes(plan_name: str, kind: str):
     return out
 
 
-def traffic(rep: str, kind: str, plan_name: str, out: str) -> None:
+def traffic(rep: str, kind: str, plan_name: str, out: str, layer: int = 0) -> None:
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = [r for r in rows_of(raw) if r.get("ID", "").isdigit()]
-    ops = alg_bytes(plan_name, kind)
+    ops = alg_bytes(plan_name, kind, layer)
     got = []
     for r, op in zip(rows[:4], ops):
         rd = float(r["dram__bytes_read.sum"].replace(",", ""))
@@ -140,7 +147,7 @@ def traffic(rep: str, kind: str, plan_name: str, out: str) -> None:
         g["dram_write"] *= scale_w
         g["duration_ns"] *= tscale
         g["traffic_over_alg"] = (g["dram_read"] + g["dram_write"]) / g["alg_bytes"]
-    entry = {"source": f"profiles/{Path(rep).stem}.ncu-rep (ncu --set full, bench.py timed round)",
+    entry = {"source": f"profiles/{Path(rep).stem}.ncu-rep (ncu --set full, bench.py timed round, layer {layer})",
              "launches": len(got),
              "dram_bytes_per_launch": sum(g["dram_read"] + g["dram_write"] for g in got) / len(got),
              "alg_bytes_per_launch": sum(g["alg_bytes"] for g in got) / len(got),
@@ -158,6 +165,7 @@ if __name__ == "__main__":
         launches(a[1], a[2], a[3] if len(a) > 3 else None)
     elif a[0] == "traffic":
         out = a[a.index("--out") + 1] if "--out" in a else str(ROOT / "profiles" / "ncu_traffic.json")
-        traffic(a[1], a[2], a[3], out)
+        layer = int(a[a.index("--layer") + 1]) if "--layer" in a else 0
+        traffic(a[1], a[2], a[3], out, layer)
     else:
         sys.exit(__doc__)
