@@ -60,6 +60,14 @@
 #ifndef HP_DEC_CORES
 #define HP_DEC_CORES 0
 #endif
+// stream-K straggler reduction of the CTA's final segment via bulk copies
+#ifndef HP_SK_TMA_RED
+#define HP_SK_TMA_RED 1  // 40-layer OPT-13B plan decode step 3267 -> 3152 us (round 2)
+#endif
+// dequant: slices converted before waiting for the TMEM A slot (0 = wait first)
+#ifndef HP_DQ_EARLY
+#define HP_DQ_EARLY 0
+#endif
 
 // The MMA issuer is one latency-critical warp: it spins on its barriers
 // instead of suspending (40-layer decode step -0.7%; HP_MMA_SPIN=0 restores
@@ -169,6 +177,11 @@ struct seg_iter {
         wlast = tstart > wlo ? tstart : wlo;
         w = wlast;
         phase = 0;
+    }
+    // true once the segment last returned by next() was this CTA's final one
+    // (stream-K mode)
+    __device__ __forceinline__ bool at_end() const {
+        return phase == 0 ? (w >= w1 && wlo >= wlast) : w >= wlast;
     }
     __device__ __forceinline__ bool next(const qgemm_args& a, seg_t& s) {
         if (!a.stream_k || u < a.dp) {
@@ -381,6 +394,7 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
     uint64_t* tempty = tfull + NACC;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NACC);
     unsigned* bcast = tmem_slot + 1;
+    uint64_t* redbar = reinterpret_cast<uint64_t*>(tmem_slot + 2);  // final-segment reduction
 
     // warp index broadcast from lane 0: provably warp-uniform for the
     // compiler, so role code runs on the uniform datapath (no R2UR)
@@ -413,6 +427,7 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 4);
         }
+        mbar_init(redbar, 1);
         fence_mbar_init();
     }
     if (warp == 3 && lane == 0) prefetch_tmap(&tmap_x);
@@ -567,9 +582,11 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
                 if (trole >= 0) trace_ev(a, trole, it, 0);
                 DQ_WAIT(&full_c[s], (it / CR) & 1);
                 if (trole >= 0) trace_ev(a, trole, it, 1);
+#if !HP_DQ_EARLY
                 DQ_WAIT(&aempty[as], ((it / AS) & 1) ^ 1);
                 if (trole >= 0) trace_ev(a, trole, it, 2);
                 tc_fence_after();
+#endif
                 const int x0 = kh * kSl;  // first local slice of this warp
                 const int gi = x0 >> 2;
                 const uint32_t cbase = smem_u32(stage_codes(s)) + r * 16;
@@ -607,9 +624,30 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty_c[s]);
                 if (trole >= 0) trace_ev(a, 4, it, 0);
+#if HP_DQ_EARLY
+                // The TMEM A slot frees only when the MMA of this warpgroup's
+                // previous stage completes: load the codes and convert the
+                // first slice(s) before waiting for it, off the MMA's
+                // critical path.
+                constexpr int kPre = HP_DQ_EARLY;
+                uint32_t vpre[kPre][16];
+#pragma unroll
+                for (int h = 0; h < kPre; ++h)
+                    if (x0 + h < nsl)
+                        convert_slice<BITS, SYM, GS>(wv[h], sf[0], zf[0], scale_arg<SYM>(sf[0]),
+                                                     zero_arg<SYM>(sf[0], zf[0]), vpre[h]);
+                DQ_WAIT(&aempty[as], ((it / AS) & 1) ^ 1);
+                if (trole >= 0) trace_ev(a, trole, it, 2);
+                tc_fence_after();
+#pragma unroll
+                for (int h = 0; h < kPre; ++h)
+                    if (x0 + h < nsl) tmem_st16(tmem + lane_addr + C::A0 + as * C::ACOLS + (x0 + h) * 16, vpre[h]);
+#else
+                constexpr int kPre = 0;
+#endif
                 // phase 2: convert + store into the TMEM A stage
 #pragma unroll
-                for (int h = 0; h < kSl; ++h) {
+                for (int h = kPre; h < kSl; ++h) {
                     if (x0 + h < nsl) {
                         const int j = h >> 2;
                         uint32_t v[16];
@@ -740,7 +778,47 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
                 }
                 asm volatile("bar.sync 1, 128;" ::: "memory");
                 trace_ev(a, tr5, ut, 1);
-                if (*bcast == static_cast<unsigned>(sg.nseg - 1)) {
+                bool tma_red = false;
+#if HP_SK_TMA_RED
+                // The straggler's reduction is usually the CTA's FINAL segment:
+                // every MMA of the CTA has completed, so the activation ring is
+                // idle. Pull all nseg partials (16 KB each at BN = 32) into it
+                // with bulk copies -- one L2 round trip -- and sum from SMEM.
+                tma_red = *bcast == static_cast<unsigned>(sg.nseg - 1) && BN <= 32 &&
+                          sg.nseg * BN * 128 * 4 <= BR * C::kB && a.dp == 0 && iter.at_end();
+                if (tma_red) {
+                    constexpr uint32_t kSeg = BN * 128 * 4;
+                    const uint8_t* src = reinterpret_cast<const uint8_t*>(a.partial) +
+                                         static_cast<size_t>(sg.tile) * a.maxseg * kSeg;
+                    if (warp == C::kEpiWarp0) {
+                        mbar_arrive_expect_tx_elect(redbar, sg.nseg * kSeg);
+                        for (int j = 0; j < sg.nseg; ++j)
+                            bulk_g2s_elect(stage_b(0) + j * kSeg, src + j * kSeg, kSeg, redbar);
+                    }
+                    mbar_wait(redbar, 0);  // once per CTA: its final segment
+                    const float4* sp = reinterpret_cast<const float4*>(stage_b(0)) + r;
+#pragma unroll 1
+                    for (int c0 = 0; c0 < BN; c0 += 16) {
+                        float f[16];
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) f[i] = 0.f;
+#pragma unroll 1
+                        for (int j = 0; j < sg.nseg; ++j) {
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                const float4 q = sp[(static_cast<size_t>(j) * (BN / 4) + c0 / 4 + i) * 128];
+                                f[4 * i] += q.x;
+                                f[4 * i + 1] += q.y;
+                                f[4 * i + 2] += q.z;
+                                f[4 * i + 3] += q.w;
+                            }
+                        }
+                        stage_store16(a, stg, C::kStgLd, r, f, mt * BN + c0, nt * 128);
+                    }
+                    if (warp == C::kEpiWarp0 && lane == 0) a.counters[sg.tile] = 0u;
+                }
+#endif
+                if (!tma_red && *bcast == static_cast<unsigned>(sg.nseg - 1)) {
                     trace_ev(a, tr5, ut, 2);
                     // ordered reduction of all segments of this tile (row r), 16
                     // tokens at a time. The partial loads of kRB segments are
