@@ -312,7 +312,10 @@ __global__ void __launch_bounds__(128)
                        __nv_bfloat16* __restrict__ out, __nv_bfloat16* __restrict__ kc,
                        __nv_bfloat16* __restrict__ vc, int req0, int S_max) {
     constexpr int EL = D / 32;  // dims per lane (2 or 4)
-    constexpr int KU = 8;       // keys per chunk: 2*KU row loads in flight per lane
+#ifndef HP_ATTN_KU
+#define HP_ATTN_KU 8
+#endif
+    constexpr int KU = HP_ATTN_KU;  // keys per chunk: 2*KU row loads in flight per lane
     using raw_t = typename std::conditional<EL == 4, uint2, uint32_t>::type;
     __shared__ float s_m[4], s_l[4];
     __shared__ float s_acc[4][D];

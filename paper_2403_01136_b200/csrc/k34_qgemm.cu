@@ -510,9 +510,9 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
                 for (int sl = 4 * sg.g0; sl < 4 * sg.g1; sl += SPS, ++it) {
                     const int nsl = min(SPS, 4 * sg.g1 - sl);
                     const int s = it % BR, as = it % AS, slot = it & 1;
-                    mbar_wait_warp(&tempty[slot], ((it >> 1) & 1) ^ 1);
-                    mbar_wait_warp(&full_b[s], (it / BR) & 1);
-                    mbar_wait_warp(&afull[as], (it / AS) & 1);
+                    MMA_WAIT(&tempty[slot], ((it >> 1) & 1) ^ 1);
+                    MMA_WAIT(&full_b[s], (it / BR) & 1);
+                    MMA_WAIT(&afull[as], (it / AS) & 1);
                     tc_fence_after();
                     const uint32_t bbase = smem_u32(stage_b(s));
                     const uint32_t abase = tmem + C::A0 + as * C::ACOLS;
@@ -659,8 +659,11 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
                 if (trole >= 0) trace_ev(a, 4, it, 1);
                 tmem_st_wait();
                 if (trole >= 0) trace_ev(a, 4, it, 2);
+#ifndef HP_EXP_NOFENCE  // timing experiment only
                 tc_fence_before();
+#endif
                 __syncwarp();
+                if (trole >= 0) trace_ev(a, 4, it, 3);
                 if (lane == 0) mbar_arrive(&afull[as]);
                 if (trole >= 0) trace_ev(a, trole, it, 3);
             }
@@ -677,17 +680,29 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
             const int acc = ut % NACC;
             constexpr bool kSK = true;  // stream-K: decode tiles, and wave-quantised prefill ops
             if constexpr (GS) {
-                // fold each stage's group sums into registers: acc += s_g * sum_g
+                // fold each stage's group sums into registers: acc += s_g * sum_g.
+                // The group scales come from global memory one stage ahead
+                // (their L2 latency hidden behind the current stage's folds).
                 float fa[BN];
 #pragma unroll
                 for (int i = 0; i < BN; ++i) fa[i] = 0.f;
+                auto load_sc = [&](int sl, float* sc) {
+                    const int g = sl >> 2;
+                    const int ng = min(C::NG, sg.g1 - g);
+#pragma unroll
+                    for (int j = 0; j < C::NG; ++j)
+                        sc[j] = (sl < 4 * sg.g1 && j < ng)
+                                    ? __ldg(a.scale + (static_cast<size_t>(nt) * a.G + g + j) * 128 + r) : 0.f;
+                };
+                float scn[C::NG];
+                load_sc(4 * sg.g0, scn);
                 for (int sl = 4 * sg.g0; sl < 4 * sg.g1; sl += SPS, ++git) {
                     const int g = sl >> 2;
                     const int ng = min(C::NG, sg.g1 - g);
                     float sc[C::NG];
 #pragma unroll
-                    for (int j = 0; j < C::NG; ++j)
-                        sc[j] = j < ng ? __ldg(a.scale + (static_cast<size_t>(nt) * a.G + g + j) * 128 + r) : 0.f;
+                    for (int j = 0; j < C::NG; ++j) sc[j] = scn[j];
+                    load_sc(sl + SPS, scn);
                     const int slot = git & 1;
                     mbar_wait(&tfull[slot], (git >> 1) & 1);
                     tc_fence_after();
