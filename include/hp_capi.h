@@ -154,15 +154,19 @@ hp_status hp_layernorm(const void* x, int64_t ldx, int64_t rows, int64_t h, cons
  *    requests req0.. ; out [reqs*s x h].
  *  hp_attention_decode: one query row per request (rows = requests
  *    req0..), appends K/V at position p, attends over cache rows 0..p;
- *    s + n <= 1024.
+ *    split > 1 cuts the context into `split` CTAs per (request, head) whose
+ *    partials merge deterministically (workspace of
+ *    hp_attention_decode_workspace_bytes, zeroed once, self-resetting).
  *  hp_argmax: tok[r] = argmax_v logits[r][v] (ties -> lowest id), int32.  */
 hp_status hp_embed(const int32_t* tok, int rows, int pos0, int pos_per_req, int s_tokens,
                    const void* E, const void* P, int64_t pos_s, int64_t h, int64_t vocab, void* x,
                    hp_stream stream);
 hp_status hp_attention_prefill(const void* qkv, int reqs, int s, int64_t h, int hd, void* out,
                                void* k_cache, void* v_cache, int req0, int s_max, hp_stream stream);
+size_t hp_attention_decode_workspace_bytes(int rows, int64_t h, int hd, int split);
 hp_status hp_attention_decode(const void* qkv, int rows, int64_t h, int hd, int p, void* out,
-                              void* k_cache, void* v_cache, int req0, int s_max, hp_stream stream);
+                              void* k_cache, void* v_cache, int req0, int s_max, int split,
+                              void* workspace, size_t ws_bytes, hp_stream stream);
 hp_status hp_argmax(const void* logits, int64_t ld, int rows, int64_t vocab, int32_t* tok,
                     hp_stream stream);
 

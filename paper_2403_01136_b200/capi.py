@@ -131,7 +131,8 @@ def _load() -> C.CDLL:
         "hp_layernorm": (i32, [v, i64, i64, i64, v, v, v, i64, v]),
         "hp_embed": (i32, [v, i32, i32, i32, i32, v, v, i64, i64, i64, v, v]),
         "hp_attention_prefill": (i32, [v, i32, i32, i64, i32, v, v, v, i32, i32, v]),
-        "hp_attention_decode": (i32, [v, i32, i64, i32, i32, v, v, v, i32, i32, v]),
+        "hp_attention_decode_workspace_bytes": (C.c_size_t, [i32, i64, i32, i32]),
+        "hp_attention_decode": (i32, [v, i32, i64, i32, i32, v, v, v, i32, i32, i32, v, C.c_size_t, v]),
         "hp_argmax": (i32, [v, i64, i32, i64, v, v]),
     })
     optional = {}
@@ -156,7 +157,7 @@ EXPORTED = [
     "hp_host_make_schedule", "hp_host_simulate", "hp_host_plan_check", "hp_host_unit_order", "hp_host_latency_fit", "hp_host_latency_predict", "hp_set_sm_budget", "hp_set_pdl",
     "hp_nccl_unique_id", "hp_pipeline_create", "hp_pipeline_run", "hp_pipeline_stage_costs",
     "hp_pipeline_kernel_stats", "hp_pipeline_layer_costs", "hp_pipeline_info", "hp_pipeline_destroy",
-    "hp_layernorm", "hp_embed", "hp_attention_prefill", "hp_attention_decode", "hp_argmax",
+    "hp_layernorm", "hp_embed", "hp_attention_prefill", "hp_attention_decode", "hp_attention_decode_workspace_bytes", "hp_argmax",
     "hp_pipeline_final_hidden", "hp_pipeline_load_stats", "hp_mbm_create", "hp_mbm_prefill_done",
     "hp_mbm_decode_done", "hp_mbm_next", "hp_mbm_destroy",
 ]

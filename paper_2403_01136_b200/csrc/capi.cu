@@ -50,7 +50,8 @@ cudaError_t launch_embed(const int32_t* tok, int rows, int pos0, int pos_per_req
 cudaError_t launch_attn_prefill(const void* qkv, int reqs, int s, int h, int D, void* out, void* kc,
                                 void* vc, int req0, int S_max, cudaStream_t st);
 cudaError_t launch_attn_decode(const void* qkv, int rows, int h, int D, int p, void* out, void* kc,
-                               void* vc, int req0, int S_max, cudaStream_t st);
+                               void* vc, int req0, int S_max, cudaStream_t st, void* ws, int split);
+size_t attn_decode_workspace(int rows, int h, int D, int split);
 cudaError_t launch_argmax(const void* logits, int64_t ld, int rows, int64_t vocab, int32_t* tok,
                           int32_t* tok2, int64_t tok2_stride, cudaStream_t st);
 cudaError_t launch_qgemm(const CUtensorMap& map, const qgemm_plan& p, int bits, bool sym,
@@ -366,14 +367,23 @@ hp_status hp_attention_prefill(const void* qkv, int reqs, int s, int64_t h, int 
                        "attention_prefill");
 }
 
+size_t hp_attention_decode_workspace_bytes(int rows, int64_t h, int hd, int split) {
+    if ((hd != 64 && hd != 128) || h % hd || rows <= 0 || split < 1) return 0;
+    return hp::attn_decode_workspace(rows, static_cast<int>(h), hd, split);
+}
+
 hp_status hp_attention_decode(const void* qkv, int rows, int64_t h, int hd, int p, void* out,
-                              void* k_cache, void* v_cache, int req0, int s_max, hp_stream stream) {
+                              void* k_cache, void* v_cache, int req0, int s_max, int split,
+                              void* workspace, size_t ws_bytes, hp_stream stream) {
     if (!qkv || !out || !k_cache || !v_cache) return fail(HP_EINVAL, "attention_decode: NULL pointer");
-    if ((hd != 64 && hd != 128) || h % hd || rows <= 0 || p < 0 || p >= s_max || s_max > 1024 || req0 < 0)
-        return fail(HP_EINVAL, "attention_decode: bad shape (head dim 64 or 128, s_max <= 1024)");
+    if ((hd != 64 && hd != 128) || h % hd || rows <= 0 || p < 0 || p >= s_max || req0 < 0 || split < 1 || split > 8)
+        return fail(HP_EINVAL, "attention_decode: bad shape (head dim 64 or 128, split 1..8)");
+    if (split > 1 && (!workspace || ws_bytes < hp::attn_decode_workspace(rows, static_cast<int>(h), hd, split)))
+        return fail(HP_EINVAL, "attention_decode: split > 1 needs hp_attention_decode_workspace_bytes of zeroed workspace");
     if (hp_status st = need_device()) return st;
     return cuda_status(hp::launch_attn_decode(qkv, rows, static_cast<int>(h), hd, p, out, k_cache,
-                                              v_cache, req0, s_max, static_cast<cudaStream_t>(stream)),
+                                              v_cache, req0, s_max, static_cast<cudaStream_t>(stream),
+                                              workspace, split),
                        "attention_decode");
 }
 

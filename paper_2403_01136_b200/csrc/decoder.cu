@@ -310,7 +310,8 @@ template <int D>
 __global__ void __launch_bounds__(128)
     attn_decode_kernel(const __nv_bfloat16* __restrict__ qkv, int h, int p, float scale_log2,
                        __nv_bfloat16* __restrict__ out, __nv_bfloat16* __restrict__ kc,
-                       __nv_bfloat16* __restrict__ vc, int req0, int S_max) {
+                       __nv_bfloat16* __restrict__ vc, int req0, int S_max,
+                       float* __restrict__ part, unsigned* __restrict__ tickets) {
     constexpr int EL = D / 32;  // dims per lane (2 or 4)
 #ifndef HP_ATTN_KU
 #define HP_ATTN_KU 8
@@ -321,7 +322,7 @@ __global__ void __launch_bounds__(128)
     __shared__ float s_acc[4][D];
     pdl_wait_glue();
     pdl_trigger_glue();
-    const int head = blockIdx.x, r = blockIdx.y;
+    const int head = blockIdx.x, r = blockIdx.y, z = blockIdx.z, nz = gridDim.z;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t ld = 3LL * h;
     const __nv_bfloat16* row = qkv + static_cast<int64_t>(r) * ld + head * D;
@@ -329,7 +330,7 @@ __global__ void __launch_bounds__(128)
     float q[EL];
 #pragma unroll
     for (int e = 0; e < EL; ++e) q[e] = __bfloat162float(row[lane * EL + e]) * scale_log2;
-    if (warp == 0) {  // append k/v at p
+    if (warp == 0 && z == nz - 1) {  // append k/v at p (the split that reads row p)
 #pragma unroll
         for (int e = 0; e < EL; ++e) {
             kc[cbase + static_cast<int64_t>(p) * h + lane * EL + e] = row[h + lane * EL + e];
@@ -337,7 +338,9 @@ __global__ void __launch_bounds__(128)
         }
     }
     __syncthreads();  // the new row is visible to the CTA (same-CTA global RAW)
-    const int nk = p + 1;
+    // this split's keys [k_lo, k_hi) of 0..p
+    const int k_lo = static_cast<int>((static_cast<int64_t>(p + 1) * z) / nz);
+    const int nk = static_cast<int>((static_cast<int64_t>(p + 1) * (z + 1)) / nz);
     auto unpack = [&](raw_t v, float* f) {
         if constexpr (EL == 4) {
             const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.x));
@@ -351,7 +354,7 @@ __global__ void __launch_bounds__(128)
     float m = -FLT_MAX, l = 0.f, acc[EL];
 #pragma unroll
     for (int e = 0; e < EL; ++e) acc[e] = 0.f;
-    for (int k0 = warp * KU; k0 < nk; k0 += 4 * KU) {
+    for (int k0 = k_lo + warp * KU; k0 < nk; k0 += 4 * KU) {
         raw_t kr[KU], vr[KU];
 #pragma unroll
         for (int u = 0; u < KU; ++u) {
@@ -399,17 +402,53 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
     for (int e = 0; e < EL; ++e) s_acc[warp][lane * EL + e] = acc[e];
     __syncthreads();
+    const float M = fmaxf(fmaxf(s_m[0], s_m[1]), fmaxf(s_m[2], s_m[3]));
+    float L = 0.f, v = 0.f;
     if (tid < D) {
-        const float M = fmaxf(fmaxf(s_m[0], s_m[1]), fmaxf(s_m[2], s_m[3]));
-        float L = 0.f, v = 0.f;
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
             const float c = s_m[w] == -FLT_MAX ? 0.f : exp2f(s_m[w] - M);  // empty warp: no keys
             L += s_l[w] * c;
             v += s_acc[w][tid] * c;
         }
-        out[static_cast<int64_t>(r) * h + head * D + tid] = __float2bfloat16_rn(v / L);
     }
+    const int64_t orow = static_cast<int64_t>(r) * h + head * D;
+    if (nz == 1) {
+        if (tid < D) out[orow + tid] = __float2bfloat16_rn(v / L);
+        return;
+    }
+    // split context: publish (M, L, acc) of this split; the last of the nz
+    // CTAs of (row, head) merges them in split order (deterministic)
+    const int64_t pair = static_cast<int64_t>(r) * gridDim.x + head;
+    float* mine = part + (pair * nz + z) * (D + 2);
+    if (tid < D) mine[2 + tid] = v;
+    if (tid == 0) {
+        mine[0] = M;
+        mine[1] = L;
+    }
+    __shared__ unsigned s_old;
+    __syncthreads();  // all of this CTA's partial stores precede the ticket (release below)
+    if (tid == 0) {
+        unsigned old;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(tickets + pair) : "memory");
+        s_old = old;
+    }
+    __syncthreads();
+    if (s_old != static_cast<unsigned>(nz - 1)) return;
+    if (tid < D) {
+        const float* base = part + pair * nz * (D + 2);
+        float MM = -FLT_MAX;
+        for (int j = 0; j < nz; ++j) MM = fmaxf(MM, __ldcg(base + j * (D + 2)));
+        float LL = 0.f, VV = 0.f;
+        for (int j = 0; j < nz; ++j) {
+            const float mj = __ldcg(base + j * (D + 2));
+            const float c = mj == -FLT_MAX ? 0.f : exp2f(mj - MM);
+            LL += __ldcg(base + j * (D + 2) + 1) * c;
+            VV += __ldcg(base + j * (D + 2) + 2 + tid) * c;
+        }
+        out[orow + tid] = __float2bfloat16_rn(VV / LL);
+    }
+    if (tid == 0) tickets[pair] = 0u;  // self-resetting for the next launch
 }
 
 // ------------------------------------------------------------------ argmax
@@ -511,16 +550,30 @@ cudaError_t launch_attn_prefill(const void* qkv, int reqs, int s, int h, int D, 
     return launch_ex(fn, grid, dim3(32 * kPrefillWarps), smem, st, args);
 }
 
+// Split-context scratch for launch_attn_decode: fp32 (M, L, acc[D]) per
+// (row, head, split) + a self-resetting ticket per (row, head); zero once.
+size_t attn_decode_workspace(int rows, int h, int D, int split) {
+    if (split <= 1) return 0;
+    const size_t pairs = static_cast<size_t>(rows) * (h / D);
+    return pairs * split * (D + 2) * sizeof(float) + pairs * sizeof(unsigned);
+}
+
 cudaError_t launch_attn_decode(const void* qkv, int rows, int h, int D, int p, void* out, void* kc,
-                               void* vc, int req0, int S_max, cudaStream_t st) {
+                               void* vc, int req0, int S_max, cudaStream_t st, void* ws, int split) {
     if (p + 1 > 1024) return cudaErrorInvalidValue;  // s_sc holds the row's scores
     const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(D));
     const __nv_bfloat16* q = static_cast<const __nv_bfloat16*>(qkv);
     __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out);
     __nv_bfloat16* k = static_cast<__nv_bfloat16*>(kc);
     __nv_bfloat16* v = static_cast<__nv_bfloat16*>(vc);
-    void* args[] = {&q, &h, &p, const_cast<float*>(&scale_log2), &o, &k, &v, &req0, &S_max};
-    const dim3 grid(h / D, rows);
+    if (split < 1 || (split > 1 && !ws)) split = 1;
+    float* part = static_cast<float*>(ws);
+    unsigned* tick = split > 1 ? reinterpret_cast<unsigned*>(
+                                     static_cast<char*>(ws) +
+                                     static_cast<size_t>(rows) * (h / D) * split * (D + 2) * sizeof(float))
+                               : nullptr;
+    void* args[] = {&q, &h, &p, const_cast<float*>(&scale_log2), &o, &k, &v, &req0, &S_max, &part, &tick};
+    const dim3 grid(h / D, rows, split);
     if (D == 128) return launch_ex(reinterpret_cast<const void*>(attn_decode_kernel<128>), grid, dim3(128), 0, st, args);
     if (D == 64) return launch_ex(reinterpret_cast<const void*>(attn_decode_kernel<64>), grid, dim3(128), 0, st, args);
     return cudaErrorInvalidValue;

@@ -47,7 +47,8 @@ cudaError_t launch_embed(const int32_t* tok, int rows, int pos0, int pos_per_req
 cudaError_t launch_attn_prefill(const void* qkv, int reqs, int s, int h, int D, void* out, void* kc,
                                 void* vc, int req0, int S_max, cudaStream_t st);
 cudaError_t launch_attn_decode(const void* qkv, int rows, int h, int D, int p, void* out, void* kc,
-                               void* vc, int req0, int S_max, cudaStream_t st);
+                               void* vc, int req0, int S_max, cudaStream_t st, void* ws, int split);
+size_t attn_decode_workspace(int rows, int h, int D, int split);
 cudaError_t launch_argmax(const void* logits, int64_t ld, int rows, int64_t vocab, int32_t* tok,
                           int32_t* tok2, int64_t tok2_stride, cudaStream_t st);
 cudaError_t launch_synth_tokens(int32_t* out, int64_t n, uint64_t seed, int64_t vocab,
@@ -318,6 +319,9 @@ struct pipeline::impl {
     std::vector<void*> dec_x;    // per group [xi_g x h1]
     void* ws = nullptr;
     size_t ws_bytes = 0;
+    // decode attention: context split over 2 CTAs per (request, head)
+    static constexpr int kAttnSplit = 2;
+    void* attn_ws = nullptr;
     int64_t weight_bytes = 0;
     load_stats lstats;
 
@@ -502,7 +506,6 @@ struct pipeline::impl {
         if (hd != 64 && hd != 128)
             throw std::invalid_argument("pipeline: attention head dim must be 64 or 128 (h1 / num_heads = " +
                                         std::to_string(hd) + ")");
-        if (S_max > 1024) throw std::invalid_argument("pipeline: s + n must be <= 1024");
         if (vocab <= 0 || vocab > (int64_t(1) << 31)) throw std::invalid_argument("pipeline: bad vocab_s");
         sched = pipesim::make_schedule(B, eta, xi);
         for (int g = 0; g < sched.num_groups; ++g) {
@@ -589,6 +592,10 @@ struct pipeline::impl {
         if (ws_bytes) {
             ws = alloc(ws_bytes);
             cuda_ok(cudaMemsetAsync(ws, 0, ws_bytes, cs), "ws");
+        }
+        if (const size_t ab = hp::attn_decode_workspace(xi, static_cast<int>(h1), hd, kAttnSplit)) {
+            attn_ws = alloc(ab);
+            cuda_ok(cudaMemsetAsync(attn_ws, 0, ab, cs), "attention ws");
         }
 
         load_kernels();
@@ -678,7 +685,8 @@ struct pipeline::impl {
                         "attention (prefill)");
             } else {
                 cuda_ok(hp::launch_attn_decode(scr_qkv, u.nreq, static_cast<int>(h1), hd, u.pos, scr_a,
-                                               kcache(L), vcache(L), u.req0, S_max, cs),
+                                               kcache(L), vcache(L), u.req0, S_max, cs, attn_ws,
+                                               kAttnSplit),
                         "attention (decode)");
             }
             record(ev, 8);
@@ -1090,7 +1098,7 @@ struct pipeline::impl {
         }
         for (void* p : {embed, pos_emb, static_cast<void*>(prompt_tok), static_cast<void*>(pristine_tok),
                         lnf[0], lnf[1], lm.packed, lm_x, lm_a, logits, static_cast<void*>(out_tok),
-                        static_cast<void*>(cur_tok), prompt, scr_a, scr_qkv, scr_f, ws})
+                        static_cast<void*>(cur_tok), prompt, scr_a, scr_qkv, scr_f, ws, attn_ws})
             f(p);
         for (void* p : dec_x) f(p);
         for (auto* v : {&unit_ev, &recv_ev, &comp_ev, &op_ev[0], &op_ev[1], &lay_ev[0], &lay_ev[1]})

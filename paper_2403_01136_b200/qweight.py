@@ -193,12 +193,22 @@ def attention_prefill(qkv: torch.Tensor, reqs: int, s: int, hd: int, kc: torch.T
     return out
 
 
+_attn_ws: dict = {}
+
+
 def attention_decode(qkv: torch.Tensor, hd: int, p: int, kc: torch.Tensor, vc: torch.Tensor,
-                     req0: int, s_max: int, stream=None) -> torch.Tensor:
+                     req0: int, s_max: int, split: int = 1, stream=None) -> torch.Tensor:
     rows, h = qkv.shape[0], qkv.shape[1] // 3
     out = torch.empty(rows, h, dtype=torch.bfloat16, device=qkv.device)
+    need = int(lib.hp_attention_decode_workspace_bytes(rows, h, hd, split))
+    ws = None
+    if need:
+        key = str(qkv.device)
+        if key not in _attn_ws or _attn_ws[key].numel() < need:
+            _attn_ws[key] = torch.zeros(need, dtype=torch.uint8, device=qkv.device)
+        ws = _attn_ws[key]
     check(lib.hp_attention_decode(qkv.data_ptr(), rows, h, hd, p, out.data_ptr(), kc.data_ptr(),
-                                  vc.data_ptr(), req0, s_max, _stream(stream)))
+                                  vc.data_ptr(), req0, s_max, split, _ptr(ws), need, _stream(stream)))
     return out
 
 

@@ -54,6 +54,11 @@ CONFIGS = {
                                     group=1, omega="survey", latency="b200_opt13b"),
     "opt30b_b32_1gpu_b200lat": dict(model="opt-30b", devices=1, mem=44 * GiB, B=32, supported=None,
                                     group=1, omega="survey", latency="b200_opt30b"),
+    "opt66b_b32_8gpu_b200lat": dict(model="opt-66b", devices=8, mem=12 * GiB, B=32, supported=[4, 8],
+                                    group=2, omega="survey", latency="b200_opt66b"),
+    "bloom176b_b32_8gpu_b200lat": dict(model="bloom-176b", devices=8, mem=24 * GiB, B=32,
+                                       supported=[3, 4, 8], group=2, omega="survey",
+                                       latency="b200_bloom176b"),
     "opt30b_b32_2gpu": dict(model="opt-30b", devices=2, mem=24 * GiB, B=32, supported=None,
                             group=2, omega="survey"),
     "opt30b_b32_4gpu": dict(model="opt-30b", devices=4, mem=12 * GiB, B=32, supported=None,

@@ -49,8 +49,9 @@ def test_prefill_attention_and_cache_write(cuda, hd, heads, s):
     assert torch.count_nonzero(kc[0]) == 0 and torch.count_nonzero(kc[req0:req0 + reqs, s:]) == 0
 
 
+@pytest.mark.parametrize("split", [1, 2, 3])
 @pytest.mark.parametrize("hd,heads,p", [(128, 40, 611), (64, 12, 512), (128, 2, 0), (64, 3, 33)])
-def test_decode_attention_appends_and_attends(cuda, hd, heads, p):
+def test_decode_attention_appends_and_attends(cuda, hd, heads, p, split):
     import torch
     from paper_2403_01136_b200 import qweight
     g = torch.Generator(device=cuda).manual_seed(hd * 7 + p)
@@ -60,8 +61,10 @@ def test_decode_attention_appends_and_attends(cuda, hd, heads, p):
     qkv = torch.randn(rows, 3 * h, generator=g, device=cuda).to(torch.bfloat16)
     req0 = 2
     k_before = kc.clone()
-    out = qweight.attention_decode(qkv, hd, p, kc, vc, req0, S_max)
+    out = qweight.attention_decode(qkv, hd, p, kc, vc, req0, S_max, split=split)
     torch.cuda.synchronize()
+    if split > 1:  # deterministic merge of the splits: a rerun gives the same bits
+        assert torch.equal(out, qweight.attention_decode(qkv, hd, p, kc, vc, req0, S_max, split=split))
     for r in range(rows):
         assert torch.equal(kc[req0 + r, p], qkv[r, h:2 * h])
         assert torch.equal(vc[req0 + r, p], qkv[r, 2 * h:])

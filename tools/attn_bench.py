@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--p", type=int, default=560)
     ap.add_argument("--heads", type=int, default=40)
     ap.add_argument("--rows", type=int, default=32)
+    ap.add_argument("--split", type=int, default=2)
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     hd, S = 128, 612
@@ -30,11 +31,11 @@ def main():
     st = torch.cuda.Stream()
     with torch.cuda.stream(st):
         for kc, vc in caches:
-            qweight.attention_decode(qkv, hd, args.p, kc, vc, 0, S, stream=st)
+            qweight.attention_decode(qkv, hd, args.p, kc, vc, 0, S, split=args.split, stream=st)
         st.synchronize()
         with torch.cuda.graph(g, stream=st):
             for kc, vc in caches:
-                qweight.attention_decode(qkv, hd, args.p, kc, vc, 0, S, stream=st)
+                qweight.attention_decode(qkv, hd, args.p, kc, vc, 0, S, split=args.split, stream=st)
     g.replay()
     torch.cuda.synchronize()
     ts = []
@@ -48,7 +49,7 @@ def main():
     t = sorted(ts)[2]
     byts = 2.0 * 2 * args.rows * (args.p + 1) * h
     peaks = json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").read_text())
-    print(json.dumps({"p": args.p, "us": t * 1e6, "GBs": byts / t / 1e9, "frac": byts / t / 1e9 / peaks["hbm_gbs"]}))
+    print(json.dumps({"p": args.p, "split": args.split, "us": t * 1e6, "GBs": byts / t / 1e9, "frac": byts / t / 1e9 / peaks["hbm_gbs"]}))
 
 
 if __name__ == "__main__":

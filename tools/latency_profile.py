@@ -26,7 +26,8 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
 PRESETS = {"opt-13b": (5120, 20480, 40), "opt-30b": (7168, 28672, 56),
-           "opt-66b": (9216, 36864, 72), "opt-125m": (768, 3072, 12)}
+           "opt-66b": (9216, 36864, 72), "bloom-176b": (14336, 57344, 112),
+           "opt-125m": (768, 3072, 12)}
 
 
 def main():
@@ -70,6 +71,9 @@ def main():
         kc = torch.randn(nreq, S_max, h1, device=dev).to(torch.bfloat16)
         vc = torch.randn(nreq, S_max, h1, device=dev).to(torch.bfloat16)
         stream = lambda: torch.cuda.current_stream().cuda_stream
+        # the executor's decode attention splits the context over 2 CTAs
+        aws_n = int(lib.hp_attention_decode_workspace_bytes(vmax_dec, h1, hd, 2))
+        aws = torch.zeros(max(aws_n, 1), dtype=torch.uint8, device=dev)
 
         def stack(v, s, t, phase):
             m = v * s if phase == capi.HP_PREFILL else v
@@ -82,7 +86,8 @@ def main():
                                                    kc.data_ptr(), vc.data_ptr(), 0, S_max, stream()))
                 else:
                     check(lib.hp_attention_decode(qkv.data_ptr(), v, h1, hd, s + t - 1, a.data_ptr(),
-                                                  kc.data_ptr(), vc.data_ptr(), 0, S_max, stream()))
+                                                  kc.data_ptr(), vc.data_ptr(), 0, S_max, 2,
+                                                  aws.data_ptr(), aws_n, stream()))
                 qweight.qlinear(ops[1], a[:m], phase=phase, out=x[:m], residual=x[:m])
                 check(lib.hp_layernorm(x.data_ptr(), h1, m, h1, ln[2].data_ptr(), ln[3].data_ptr(),
                                        a.data_ptr(), h1, stream()))
