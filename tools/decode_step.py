@@ -41,6 +41,7 @@ def main():
     ap.add_argument("--m", type=int, default=32)
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--per-op", action="store_true")
+    ap.add_argument("--no-ln", action="store_true", help="timing experiment: skip the two LayerNorms")
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     h1, h2, m = args.h1, args.h2, args.m
@@ -67,12 +68,14 @@ def main():
 
     def step():
         for ops, ln in layers:
-            check(lib.hp_layernorm(xp.data_ptr(), h1, m, h1, ln[0].data_ptr(), ln[1].data_ptr(),
-                                   a.data_ptr(), h1, torch.cuda.current_stream().cuda_stream))
+            if not args.no_ln:
+                check(lib.hp_layernorm(xp.data_ptr(), h1, m, h1, ln[0].data_ptr(), ln[1].data_ptr(),
+                                       a.data_ptr(), h1, torch.cuda.current_stream().cuda_stream))
             qweight.qlinear(ops[0], a, out=qkv)
             qweight.qlinear(ops[1], qkv[:, 2 * h1:], out=xp, residual=xp)
-            check(lib.hp_layernorm(xp.data_ptr(), h1, m, h1, ln[2].data_ptr(), ln[3].data_ptr(),
-                                   a.data_ptr(), h1, torch.cuda.current_stream().cuda_stream))
+            if not args.no_ln:
+                check(lib.hp_layernorm(xp.data_ptr(), h1, m, h1, ln[2].data_ptr(), ln[3].data_ptr(),
+                                       a.data_ptr(), h1, torch.cuda.current_stream().cuda_stream))
             qweight.qlinear(ops[2], a, out=f, relu=True)
             qweight.qlinear(ops[3], f, out=xp, residual=xp)
 
