@@ -9,9 +9,10 @@
 // SPEC.md:328); stochastic rounding uses a sequential mt19937_64 stream in
 // the reference (indicator.cpp:37,50) and is rejected here.
 //
-// Fast path: x = ((float)w - (float)zero) * rcp_f32(step). Its absolute
-// error is < 1e-4 for |x| <= 255, so whenever frac(x + 0.5)
-// lies in [1e-3, 1 - 1e-3] the rounded code equals the reference's; other
+// Fast path: x = fma((float)w - (float)zero, rcp_f32(step)), the product
+// unrounded before the round-to-integer. Its absolute error is < 1e-4 for
+// |x| <= 255, so whenever frac(x + 0.5) lies in
+// [1e-3, 1 - 1e-3] the rounded code equals the reference's; other
 // elements (ties, near-ties, non-finite) take the exact fp64 sequence
 // __dsub_rn / __ddiv_rn / __dadd_rn / floor / clamp. About 0.3% of bf16
 // weights take the slow path.
@@ -60,8 +61,9 @@ __device__ __forceinline__ group_grid make_grid(float wmin, float wmax,
 }
 
 // Signed grid code of one element on the exact path: the reference's fp64
-// operation sequence (indicator.cpp:44-47) and std::clamp.
-__device__ __noinline__ int quant_code_exact(float w, double step, double zero, double lo, double hi) {
+// operation sequence (indicator.cpp:44-47) and std::clamp. Inlined into the
+// (rolled) near-tie loop: a call would spill the caller's live registers.
+__device__ __forceinline__ int quant_code_exact(float w, double step, double zero, double lo, double hi) {
     if (step == 0.0) return 0;  // flat group: out = zero (indicator.cpp:39-41)
     const double scaled = __ddiv_rn(__dsub_rn(static_cast<double>(w), zero), step);
     const double sn = floor(__dadd_rn(scaled, 0.5));
@@ -111,6 +113,46 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+#ifndef HP_K1_PAIRS
+#define HP_K1_PAIRS 1  // f32x2 fast path (round 2); 0 = the scalar round-1 path
+#endif
+
+__device__ __forceinline__ uint64_t splat2(float f) {
+    const uint64_t b = __float_as_uint(f);
+    return b | (b << 32);
+}
+
+// Fast path for the two codes of one bf16x2 word, with B200's paired fp32
+// ops (one instruction per two elements, each lane IEEE round-to-nearest):
+//   xd = x - zero_f,  nm = fma(xd, rcp_f, 1.5*2^23)  (rint of the UNROUNDED
+//   product in the low mantissa bits),  dd = fma(xd, rcp_f, 1.5*2^23 - nm)
+//   (the rounding distance; 1.5*2^23 - nm = fma(nm, -1, 1.5*2^23) is exact),
+//   e = dd*dd - T.
+// The product feeds both FMAs unrounded: ptxas contracts a separate
+// mul.rn.f32x2 + add.rn.f32x2 into FFMA2 anyway, so the scalar paths below
+// (ragged slices, the exact path's fast_bits) use the same fmaf form and all
+// three agree bit for bit.
+// e < 0 <=> |dd| < 0.5 - margin: the element is away from a tie. e >= 0 or
+// NaN (non-finite xf: canonical NaN, sign bit clear) flags it for the exact
+// fp64 path; the caller shifts the sign bits of e into a mask.
+__device__ __forceinline__ void fast_pair(uint32_t w, uint64_t nzf2, uint64_t rf2, uint64_t mg2,
+                                          uint64_t neg1, uint64_t nt2, uint32_t& nlo, uint32_t& nhi,
+                                          uint32_t& elo, uint32_t& ehi) {
+    asm("{\n\t.reg .b64 x, nm, r, dd, e;\n\t.reg .b32 lo, hi;\n\t"
+        "shl.b32 lo, %4, 16;\n\t"
+        "and.b32 hi, %4, 0xFFFF0000;\n\t"
+        "mov.b64 x, {lo, hi};\n\t"
+        "add.rn.f32x2 x, x, %5;\n\t"
+        "fma.rn.f32x2 nm, x, %6, %7;\n\t"
+        "fma.rn.f32x2 r, nm, %8, %7;\n\t"
+        "fma.rn.f32x2 dd, x, %6, r;\n\t"
+        "fma.rn.f32x2 e, dd, dd, %9;\n\t"
+        "mov.b64 {%0, %1}, nm;\n\t"
+        "mov.b64 {%2, %3}, e;\n\t}"
+        : "=r"(nlo), "=r"(nhi), "=r"(elo), "=r"(ehi)
+        : "r"(w), "l"(nzf2), "l"(rf2), "l"(mg2), "l"(neg1), "l"(nt2));
+}
 
 // Work item = (64-row block, 128-k group); one thread per (row, 32-k slice):
 // a warp covers 8 rows x one group (lane = 4 * row + slice), a 256-thread
@@ -198,6 +240,7 @@ __global__ void __launch_bounds__(256, HP_K1_CTAS)
                 v[i] = lo | (hi << 16);
             }
         }
+        const int cur = stage;  // buf[cur] stays valid until the next iteration's issue
         stage = (stage + 1) % kD;
         const int64_t nt = q.row >> 7;
         const int r = static_cast<int>(q.row & 127);
@@ -267,18 +310,18 @@ __global__ void __launch_bounds__(256, HP_K1_CTAS)
             uint32_t code15[2] = {0u, 0u};  // 3-bit pair 15 (codes 30, 31)
             // phase 1, branch-free (full ILP across the 32 codes): fast codes
             // packed, near-tie / non-finite codes flagged in `slow`
-            // __fmul_rn/__fadd_rn: no FMA contraction, so phase 2 recomputes the
+            // explicit __fmaf_rn (the pair path's FFMA2 form), so phase 2 recomputes the
             // very bits phase 1 packed
-            auto fast_bits = [&](float x) { return __float_as_uint(__fadd_rn(__fmul_rn(__fsub_rn(x, zf), rf), kMagicF)); };
+            auto fast_bits = [&](float x) { return __float_as_uint(__fmaf_rn(__fsub_rn(x, zf), rf, kMagicF)); };
             uint32_t slow = 0;
             auto phase1 = [&](auto full) {
                 constexpr bool kFull = decltype(full)::value;  // all 32 codes valid
 #pragma unroll
                 for (int e = 0; e < 32; ++e) {
                     const float x = elem(e);
-                    const float xf = __fmul_rn(__fsub_rn(x, zf), rf);
-                    const float nm = __fadd_rn(xf, kMagicF);
-                    const float d = xf - (nm - kMagicF);  // NaN for non-finite xf
+                    const float xd = __fsub_rn(x, zf);
+                    const float nm = __fmaf_rn(xd, rf, kMagicF);
+                    const float d = __fmaf_rn(xd, rf, -(nm - kMagicF));  // NaN for non-finite xf
                     uint32_t bits = __float_as_uint(nm);
                     const uint32_t flag = fabsf(d) <= 0.5f - kTieMargin ? 0u : (1u << e);
                     if (!kFull && e >= q.valid) {
@@ -293,10 +336,40 @@ __global__ void __launch_bounds__(256, HP_K1_CTAS)
                     }
                 }
             };
-            if (q.full)
+            if (q.full) {
+#if HP_K1_PAIRS
+                // ok: bit 31-e set <=> element e is away from a tie (funnel
+                // shift of the sign bit of e, one SHF per element)
+                const float tm = 0.5f - kTieMargin;
+                const uint64_t nzf2 = splat2(-zf), rf2 = splat2(rf), mg2 = splat2(kMagicF),
+                               neg1 = splat2(-1.0f), nt2 = splat2(-tm * tm);
+                uint32_t ok = 0;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    uint32_t n0, n1, e0, e1;
+                    fast_pair(v[i], nzf2, rf2, mg2, neg1, nt2, n0, n1, e0, e1);
+                    ok = __funnelshift_l(e0, ok, 1);
+                    ok = __funnelshift_l(e1, ok, 1);
+                    if (SP::split3(2 * i)) {
+                        code15[0] = n0 - kMagicBits + static_cast<uint32_t>(off);
+                        code15[1] = n1 - kMagicBits + static_cast<uint32_t>(off);
+                    } else {
+                        words[SP::word_of(2 * i)] += n0 << SP::shift_of(2 * i);
+                        words[SP::word_of(2 * i + 1)] += n1 << SP::shift_of(2 * i + 1);
+                    }
+                }
+                slow = __brev(~ok);  // bit e: element e takes the exact path
+#else
                 phase1(std::true_type{});
-            else
+#endif
+            } else {
                 phase1(std::false_type{});
+                if (slow) {  // stage the ragged slice for the exact path (own slot; no copy in flight)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        buf[cur][i][tid] = make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+                }
+            }
             // phase 2 (~0.3% of codes): the exact fp64 code replaces the fast
             // one. A rolled loop over the flagged codes (one copy of the fp64
             // sequence keeps the kernel small); registers are selected, not
@@ -304,10 +377,11 @@ __global__ void __launch_bounds__(256, HP_K1_CTAS)
             while (slow) {
                 const int e = __ffs(slow) - 1;
                 slow &= slow - 1;
-                uint32_t vw = v[0];
-#pragma unroll
-                for (int i = 1; i < 16; ++i) vw = (i == (e >> 1)) ? v[i] : vw;
-                const float x = __uint_as_float((e & 1) ? (vw & 0xFFFF0000u) : (vw << 16));
+                // the slice is in this thread's shared-memory slot (ragged
+                // slices were copied there above): no dynamically indexed
+                // register array, so nothing goes to local memory
+                const uint16_t* sb = reinterpret_cast<const uint16_t*>(&buf[cur][e >> 3][tid]);
+                const float x = __uint_as_float(static_cast<uint32_t>(sb[e & 7]) << 16);
                 const uint32_t ex = kMagicBits + static_cast<uint32_t>(
                                                      quant_code_exact(x, gg.step, gg.zero, gg.lo, gg.hi));
                 if (BITS == 3 && ((e >> 1) & 15) == 15) {
