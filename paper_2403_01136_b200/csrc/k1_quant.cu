@@ -17,6 +17,8 @@
 // __dsub_rn / __ddiv_rn / __dadd_rn / floor / clamp. About 0.3% of bf16
 // weights take the slow path.
 #include <cuda_bf16.h>
+
+#include <atomic>
 #include <cstdint>
 #include <type_traits>
 #include <utility>
@@ -114,10 +116,6 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-#ifndef HP_K1_PAIRS
-#define HP_K1_PAIRS 1  // f32x2 fast path (round 2); 0 = the scalar round-1 path
-#endif
-
 __device__ __forceinline__ uint64_t splat2(float f) {
     const uint64_t b = __float_as_uint(f);
     return b | (b << 32);
@@ -154,262 +152,253 @@ __device__ __forceinline__ void fast_pair(uint32_t w, uint64_t nzf2, uint64_t rf
         : "r"(w), "l"(nzf2), "l"(rf2), "l"(mg2), "l"(neg1), "l"(nt2));
 }
 
-// Work item = (64-row block, 128-k group); one thread per (row, 32-k slice):
-// a warp covers 8 rows x one group (lane = 4 * row + slice), a 256-thread
-// CTA 64 rows. CTAs walk items grid-stride; each thread streams its own 64
-// slice bytes into shared memory with cp.async kD-1 items ahead, so HBM
-// reads overlap the arithmetic without holding registers. The group's
-// min/max is a 2-step shuffle over the 4 lanes of a row, and each thread
-// emits exactly its slice's part of the tile layout (layout.cuh): 4-bit one
-// 16 B row entry of chunk s, 8-bit two (chunks 2s, 2s+1), 3-bit word s of
-// chunks 0..2, 16-bit four; for a fixed chunk the 8 rows of a warp are 128
-// contiguous bytes, so every store instruction writes whole lines.
-constexpr int kQRows = 64;  // rows per item
+// Work item = (128-row block, 128-k group) = one tile of the layout; two
+// threads per (row, group), each owning 64 k (slices 2h, 2h+1): a warp covers
+// 16 rows x one group (lane = 2 * row + h), a 256-thread CTA the 128 rows.
+// CTAs walk items grid-stride with an incremental (row block, group) cursor
+// (no integer division per item); each thread streams its own 128 bytes into
+// dynamic shared memory with cp.async kD-1 items ahead, so HBM reads overlap
+// the arithmetic without holding registers, and re-reads them from there per
+// pass (group min/max, then each slice). The group's min/max is one shuffle
+// with the partner lane, the fp64 grid is computed once per 64 weights, and
+// each thread emits its two slices' part of the tile layout (layout.cuh):
+// 4-bit one 16 B row entry of chunk s, 8-bit two (chunks 2s, 2s+1), 3-bit
+// word s of chunks 0..2, 16-bit four per slice; for a fixed chunk the 16
+// rows of a warp are 256 contiguous bytes.
+constexpr int kQRows = 128;  // rows per item (one tile row-block)
 #ifndef HP_K1_DEPTH
-#define HP_K1_DEPTH 3
+#define HP_K1_DEPTH 2
 #endif
 #ifndef HP_K1_CTAS
-#define HP_K1_CTAS 4  // 4 x 256 threads at 61 registers: +4-5% over 3 x 76 (round 2)
+#define HP_K1_CTAS 3  // 3 x 256 threads x 64 KB shared: +4-6% over depth 3 x 2 CTAs (round 2)
 #endif
 constexpr int kD = HP_K1_DEPTH;  // cp.async pipeline depth (items)
+constexpr int kPieces = 8;       // 16-byte pieces per thread per item (64 bf16)
+constexpr size_t kK1Smem = static_cast<size_t>(kD) * kPieces * 256 * sizeof(uint4);
 
 template <int BITS>
 __global__ void __launch_bounds__(256, HP_K1_CTAS)
-    quant_pack_kernel(const __nv_bfloat16* __restrict__ w, int64_t n_out,
-                      int64_t k_in, int64_t ldw, int G, int sym, int64_t items,
-                      uint8_t* __restrict__ packed, float* __restrict__ scale,
-                      float* __restrict__ zero, double* __restrict__ step64,
-                      double* __restrict__ zero64) {
-    __shared__ __align__(16) uint4 buf[kD][4][256];  // [stage][16 B piece][thread]
+    quant_pack_kernel(const __nv_bfloat16* __restrict__ w, int n_out, int k_in, int64_t ldw,
+                      int G, int sym, int items, uint8_t* __restrict__ packed,
+                      float* __restrict__ scale, float* __restrict__ zero,
+                      double* __restrict__ step64, double* __restrict__ zero64) {
+    extern __shared__ __align__(16) uint4 kbuf[];  // [stage][piece][thread]
     const int tid = threadIdx.x;
-    const int lane = tid & 31;
-    const int sl = lane & 3;
-    const int rin = (tid >> 5) * 8 + (lane >> 2);
+    const int h = tid & 1;     // k half of the group: slices 2h, 2h+1
+    const int rin = tid >> 1;  // row within the 128-row block
+    auto slot = [&](int st, int piece) -> uint4* { return &kbuf[(st * kPieces + piece) * 256 + tid]; };
     const bool vec_ok = (ldw % 8 == 0) && ((reinterpret_cast<uintptr_t>(w) & 15) == 0);
-    struct where {
-        int64_t row, k0;
-        int g, valid;
-        bool full;
+    // items it = blockIdx.x + j * gridDim.x as (row block, group) cursors
+    const int dq = static_cast<int>(gridDim.x) / G, dr = static_cast<int>(gridDim.x) % G;
+    auto advance = [&](int& rb, int& g) {
+        rb += dq;
+        g += dr;
+        if (g >= G) {
+            g -= G;
+            ++rb;
+        }
     };
-    auto locate = [&](int64_t it) {  // items < 2^31 (BLOOM fc1: 100k)
-        where q;
-        const uint32_t rb = static_cast<uint32_t>(it) / static_cast<uint32_t>(G);
-        q.g = static_cast<int>(static_cast<uint32_t>(it) - rb * static_cast<uint32_t>(G));
-        q.row = static_cast<int64_t>(rb) * kQRows + rin;
-        q.k0 = static_cast<int64_t>(q.g) * 128 + sl * 32;
-        const int cnt = static_cast<int>(k_in - q.k0 <= 0 ? 0 : (k_in - q.k0 < 32 ? k_in - q.k0 : 32));
-        q.valid = q.row < n_out ? cnt : 0;
-        q.full = vec_ok && q.valid == 32;
-        return q;
-    };
-    auto issue = [&](int64_t it, int stage) {
-        if (it < items) {
-            const where q = locate(it);
-            if (q.full) {
-                const __nv_bfloat16* src = w + q.row * ldw + q.k0;
+    int rb_i = static_cast<int>(blockIdx.x) / G, g_i = static_cast<int>(blockIdx.x) % G;
+    int rb_c = rb_i, g_c = g_i, it_i = blockIdx.x;
+    auto issue = [&](int st) {
+        if (it_i < items) {
+            const int row = rb_i * kQRows + rin;
+            const int k0 = g_i * 128 + h * 64;
+            if (vec_ok && row < n_out && k_in - k0 >= 64) {
+                const uint4* src = reinterpret_cast<const uint4*>(w + static_cast<int64_t>(row) * ldw + k0);
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    cp_async16(static_cast<uint32_t>(__cvta_generic_to_shared(&buf[stage][i][tid])),
-                               reinterpret_cast<const uint4*>(src) + i);
+                for (int i = 0; i < kPieces; ++i)
+                    cp_async16(static_cast<uint32_t>(__cvta_generic_to_shared(slot(st, i))), src + i);
             }
         }
         cp_async_commit();  // (possibly empty) group: keeps the wait count uniform
+        it_i += gridDim.x;
+        advance(rb_i, g_i);
     };
 
-    const int64_t step_it = gridDim.x;
 #pragma unroll
-    for (int d = 0; d < kD - 1; ++d) issue(blockIdx.x + d * step_it, d);
+    for (int d = 0; d < kD - 1; ++d) issue(d);
     int stage = 0;
-    for (int64_t it = blockIdx.x; it < items; it += step_it) {
-        issue(it + (kD - 1) * step_it, (stage + kD - 1) % kD);
+    for (int it = blockIdx.x; it < items; it += gridDim.x) {
+        issue((stage + kD - 1) % kD);
         cp_async_wait<kD - 1>();
-        const where q = locate(it);
-        uint32_t v[16];
-        if (q.full) {
+        const int rb = rb_c, g = g_c;
+        advance(rb_c, g_c);
+        const int row = rb * kQRows + rin;
+        const int k0 = g * 128 + h * 64;
+        const bool row_ok = row < n_out;
+        const int valid = row_ok ? (k_in - k0 <= 0 ? 0 : (k_in - k0 < 64 ? k_in - k0 : 64)) : 0;
+        const bool full = vec_ok && valid == 64;
+        const int cur = stage;  // slot cur stays valid until the next iteration's issue
+        stage = (stage + 1) % kD;
+        if (!full) {  // ragged k, padding rows, unaligned rows: stage zero-padded elements
+            const __nv_bfloat16* src = w + static_cast<int64_t>(row) * ldw + k0;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const uint4 u = buf[stage][i][tid];
-                v[4 * i] = u.x; v[4 * i + 1] = u.y; v[4 * i + 2] = u.z; v[4 * i + 3] = u.w;
-            }
-        } else {  // ragged k, rows past n_out (tile padding) or unaligned rows
-            const __nv_bfloat16* src = w + q.row * ldw + q.k0;
+            for (int i = 0; i < kPieces; ++i) {
+                uint32_t q4[4];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const uint32_t lo = 2 * i < q.valid ? __bfloat16_as_ushort(src[2 * i]) : 0u;
-                const uint32_t hi = 2 * i + 1 < q.valid ? __bfloat16_as_ushort(src[2 * i + 1]) : 0u;
-                v[i] = lo | (hi << 16);
+                for (int j = 0; j < 4; ++j) {
+                    const int e = 8 * i + 2 * j;
+                    const uint32_t lo = e < valid ? __bfloat16_as_ushort(src[e]) : 0u;
+                    const uint32_t hi = e + 1 < valid ? __bfloat16_as_ushort(src[e + 1]) : 0u;
+                    q4[j] = lo | (hi << 16);
+                }
+                *slot(cur, i) = make_uint4(q4[0], q4[1], q4[2], q4[3]);
             }
         }
-        const int cur = stage;  // buf[cur] stays valid until the next iteration's issue
-        stage = (stage + 1) % kD;
-        const int64_t nt = q.row >> 7;
-        const int r = static_cast<int>(q.row & 127);
-        uint8_t* tbase = packed + (static_cast<size_t>(nt) * G + q.g) * tile_bytes(BITS) + r * 16;
-        auto elem = [&](int e) { return __uint_as_float((e & 1) ? (v[e >> 1] & 0xFFFF0000u) : (v[e >> 1] << 16)); };
+        uint8_t* tbase = packed + (static_cast<size_t>(rb) * G + g) * tile_bytes(BITS) + rin * 16;
 
         if constexpr (BITS == 16) {
             // padding rows of the last tile (row >= n_out) are written as zeros
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
-                *reinterpret_cast<uint4*>(tbase + (4 * sl + c) * 2048) =
-                    make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+            for (int c = 0; c < kPieces; ++c)
+                *reinterpret_cast<uint4*>(tbase + (8 * h + c) * 2048) = *slot(cur, c);
             continue;
         } else {
-            float wmin, wmax;
-            if (q.full) {  // bf16x2 min/max (exact), halves folded at the end
-                __nv_bfloat162 mn = *reinterpret_cast<const __nv_bfloat162*>(&v[0]), mx = mn;
+            // the thread's 64 elements, read from shared memory once
+            uint32_t vv[2 * 16];
 #pragma unroll
-                for (int i = 1; i < 16; ++i) {
-                    const __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&v[i]);
-                    mn = __hmin2(mn, h);
-                    mx = __hmax2(mx, h);
+            for (int i = 0; i < kPieces; ++i) {
+                const uint4 u = *slot(cur, i);
+                vv[4 * i] = u.x; vv[4 * i + 1] = u.y; vv[4 * i + 2] = u.z; vv[4 * i + 3] = u.w;
+            }
+            float wmin, wmax;
+            if (full) {  // bf16x2 min/max (exact), halves folded at the end
+                __nv_bfloat162 mn = *reinterpret_cast<const __nv_bfloat162*>(&vv[0]), mx = mn;
+#pragma unroll
+                for (int i = 1; i < 32; ++i) {
+                    const __nv_bfloat162 hv = *reinterpret_cast<const __nv_bfloat162*>(&vv[i]);
+                    mn = __hmin2(mn, hv);
+                    mx = __hmax2(mx, hv);
                 }
                 wmin = fminf(__low2float(mn), __high2float(mn));
                 wmax = fmaxf(__low2float(mx), __high2float(mx));
             } else {
                 wmin = __int_as_float(0x7f800000);
                 wmax = -__int_as_float(0x7f800000);
-#pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    if (e < q.valid) {
-                        wmin = fminf(wmin, elem(e));
-                        wmax = fmaxf(wmax, elem(e));
-                    }
+                for (int e = 0; e < valid; ++e) {  // rolled: rare path
+                    const float x = __uint_as_float(static_cast<uint32_t>(
+                                                        reinterpret_cast<const uint16_t*>(slot(cur, e >> 3))[e & 7])
+                                                    << 16);
+                    wmin = fminf(wmin, x);
+                    wmax = fmaxf(wmax, x);
                 }
             }
             wmin = fminf(wmin, __shfl_xor_sync(0xffffffffu, wmin, 1));
             wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, 1));
-            wmin = fminf(wmin, __shfl_xor_sync(0xffffffffu, wmin, 2));
-            wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, 2));
-            const bool row_ok = q.row < n_out;
             if (!row_ok) wmin = wmax = 0.0f;
             const group_grid gg = make_grid(wmin, wmax, BITS, sym != 0);
             const int off = sym ? (1 << (BITS - 1)) - 1 : 0;
-            if (sl == 0) {
-                const size_t sidx = (static_cast<size_t>(nt) * G + q.g) * 128 + r;
+            if (h == 0) {
+                const size_t sidx = (static_cast<size_t>(rb) * G + g) * 128 + rin;
                 if (scale) scale[sidx] = row_ok ? static_cast<float>(gg.step) : 0.0f;
                 if (zero) zero[sidx] = row_ok ? gg.zero_f : 0.0f;
                 if (row_ok && step64) {
-                    step64[q.row * G + q.g] = gg.step;
-                    zero64[q.row * G + q.g] = gg.zero;
+                    step64[static_cast<int64_t>(row) * G + g] = gg.step;
+                    zero64[static_cast<int64_t>(row) * G + g] = gg.zero;
                 }
             }
-            // Fast path: xf = (w - zero) * rcp(step) in fp32 (|error| < 1e-4 for
-            // |xf| <= 255; |xf| <= hi by construction); away
-            // from a tie (|xf - rint(xf)| <= 0.5 - margin) floor(x + 0.5) ==
-            // rint(xf) and lies in [lo, hi].
-            // Near ties / non-finite values take quant_code_exact. A flat
-            // group (step 0) has rcp 0: every code is 0, as the reference.
+            // Fast path: xf = fma(w - zero, rcp(step)) in fp32 (|error| < 1e-4
+            // for |xf| <= 255; |xf| <= hi by construction);
+            // away from a tie (|xf - rint(xf)| <= 0.5 - margin) floor(x + 0.5)
+            // == rint(xf) and lies in [lo, hi]. Near ties / non-finite values
+            // take quant_code_exact. A flat group (step 0) has rcp 0: every
+            // code is 0, as the reference.
             const float zf = gg.zero_f;
             // a step below FLT_MIN is a denormal float: rcp would be inexact,
             // so NaN flags every code for the exact path
             const float rf = gg.step == 0.0 ? 0.0f : (gg.step < 1.1754943508222875e-38 ? __int_as_float(0x7fc00000) : gg.rcp_f);
             using SP = slice_pack<BITS>;
-            uint32_t words[SP::NW];
-            SP::init_words(words, sym != 0);
-            uint32_t code15[2] = {0u, 0u};  // 3-bit pair 15 (codes 30, 31)
-            // phase 1, branch-free (full ILP across the 32 codes): fast codes
-            // packed, near-tie / non-finite codes flagged in `slow`
-            // explicit __fmaf_rn (the pair path's FFMA2 form), so phase 2 recomputes the
-            // very bits phase 1 packed
+            // explicit __fmaf_rn (the pair path's FFMA2 form), so the exact
+            // path recomputes the very bits the fast path packed
             auto fast_bits = [&](float x) { return __float_as_uint(__fmaf_rn(__fsub_rn(x, zf), rf, kMagicF)); };
-            uint32_t slow = 0;
-            auto phase1 = [&](auto full) {
-                constexpr bool kFull = decltype(full)::value;  // all 32 codes valid
+            const float tm = 0.5f - kTieMargin;
+            const uint64_t nzf2 = splat2(-zf), rf2 = splat2(rf), mg2 = splat2(kMagicF),
+                           neg1 = splat2(-1.0f), nt2 = splat2(-tm * tm);
 #pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    const float x = elem(e);
-                    const float xd = __fsub_rn(x, zf);
-                    const float nm = __fmaf_rn(xd, rf, kMagicF);
-                    const float d = __fmaf_rn(xd, rf, -(nm - kMagicF));  // NaN for non-finite xf
-                    uint32_t bits = __float_as_uint(nm);
-                    const uint32_t flag = fabsf(d) <= 0.5f - kTieMargin ? 0u : (1u << e);
-                    if (!kFull && e >= q.valid) {
-                        bits = kMagicBits;  // padding: signed code 0
-                    } else {
-                        slow |= flag;
+            for (int j = 0; j < 2; ++j) {  // this thread's slices s = 2h + j
+                const int sl = 2 * h + j;
+                const uint32_t* v = vv + 16 * j;
+                const int vs = valid - 32 * j < 0 ? 0 : (valid - 32 * j > 32 ? 32 : valid - 32 * j);
+                uint32_t words[SP::NW];
+                SP::init_words(words, sym != 0);
+                uint32_t code15[2] = {0u, 0u};  // 3-bit pair 15 (codes 30, 31)
+                uint32_t slow = 0;
+                if (vs == 32) {
+                    // ok: bit 31-e set <=> element e is away from a tie (funnel
+                    // shift of the sign bit of e, one SHF per element)
+                    uint32_t ok = 0;
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        uint32_t n0, n1, e0, e1;
+                        fast_pair(v[i], nzf2, rf2, mg2, neg1, nt2, n0, n1, e0, e1);
+                        ok = __funnelshift_l(e0, ok, 1);
+                        ok = __funnelshift_l(e1, ok, 1);
+                        if (SP::split3(2 * i)) {
+                            code15[0] = n0 - kMagicBits + static_cast<uint32_t>(off);
+                            code15[1] = n1 - kMagicBits + static_cast<uint32_t>(off);
+                        } else {
+                            words[SP::word_of(2 * i)] += n0 << SP::shift_of(2 * i);
+                            words[SP::word_of(2 * i + 1)] += n1 << SP::shift_of(2 * i + 1);
+                        }
                     }
-                    if (SP::split3(e)) {
-                        code15[e & 1] = bits - kMagicBits + static_cast<uint32_t>(off);
-                    } else {
-                        words[SP::word_of(e)] += bits << SP::shift_of(e);
+                    slow = __brev(~ok);  // bit e: element e takes the exact path
+                } else {  // partial slice: scalar, padding codes are signed 0
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        const float x = __uint_as_float((e & 1) ? (v[e >> 1] & 0xFFFF0000u) : (v[e >> 1] << 16));
+                        const float xd = __fsub_rn(x, zf);
+                        const float nm = __fmaf_rn(xd, rf, kMagicF);
+                        const float d = __fmaf_rn(xd, rf, -(nm - kMagicF));  // NaN for non-finite xf
+                        uint32_t bits = __float_as_uint(nm);
+                        if (e >= vs) {
+                            bits = kMagicBits;  // padding: signed code 0
+                        } else if (!(fabsf(d) <= 0.5f - kTieMargin)) {
+                            slow |= 1u << e;
+                        }
+                        if (SP::split3(e)) {
+                            code15[e & 1] = bits - kMagicBits + static_cast<uint32_t>(off);
+                        } else {
+                            words[SP::word_of(e)] += bits << SP::shift_of(e);
+                        }
                     }
                 }
-            };
-            if (q.full) {
-#if HP_K1_PAIRS
-                // ok: bit 31-e set <=> element e is away from a tie (funnel
-                // shift of the sign bit of e, one SHF per element)
-                const float tm = 0.5f - kTieMargin;
-                const uint64_t nzf2 = splat2(-zf), rf2 = splat2(rf), mg2 = splat2(kMagicF),
-                               neg1 = splat2(-1.0f), nt2 = splat2(-tm * tm);
-                uint32_t ok = 0;
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    uint32_t n0, n1, e0, e1;
-                    fast_pair(v[i], nzf2, rf2, mg2, neg1, nt2, n0, n1, e0, e1);
-                    ok = __funnelshift_l(e0, ok, 1);
-                    ok = __funnelshift_l(e1, ok, 1);
-                    if (SP::split3(2 * i)) {
-                        code15[0] = n0 - kMagicBits + static_cast<uint32_t>(off);
-                        code15[1] = n1 - kMagicBits + static_cast<uint32_t>(off);
+                // exact fp64 path (ties, near-ties, non-finite): a rolled loop
+                // over the flagged codes, the element re-read from shared memory
+                while (slow) {
+                    const int e = __ffs(slow) - 1;
+                    slow &= slow - 1;
+                    const uint16_t* sb = reinterpret_cast<const uint16_t*>(slot(cur, 4 * j + (e >> 3)));
+                    const float x = __uint_as_float(static_cast<uint32_t>(sb[e & 7]) << 16);
+                    const uint32_t ex = kMagicBits + static_cast<uint32_t>(
+                                                         quant_code_exact(x, gg.step, gg.zero, gg.lo, gg.hi));
+                    if (BITS == 3 && ((e >> 1) & 15) == 15) {
+                        const uint32_t c = ex - kMagicBits + static_cast<uint32_t>(off);
+                        code15[0] = (e & 1) ? code15[0] : c;
+                        code15[1] = (e & 1) ? c : code15[1];
                     } else {
-                        words[SP::word_of(2 * i)] += n0 << SP::shift_of(2 * i);
-                        words[SP::word_of(2 * i + 1)] += n1 << SP::shift_of(2 * i + 1);
+                        const code_pos cp = locate_code(BITS, e);
+                        const int wi = cp.chunk * 4 + cp.word;
+                        const uint32_t delta = (ex - fast_bits(x)) << cp.shift;
+#pragma unroll
+                        for (int i = 0; i < SP::NW; ++i) words[i] += (i == wi) ? delta : 0u;
                     }
                 }
-                slow = __brev(~ok);  // bit e: element e takes the exact path
-#else
-                phase1(std::true_type{});
-#endif
-            } else {
-                phase1(std::false_type{});
-                if (slow) {  // stage the ragged slice for the exact path (own slot; no copy in flight)
+                if constexpr (BITS == 3) {
+                    // pair 15: bit b of code 30 at bit 15, of code 31 at bit 31, of chunk b
 #pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        buf[cur][i][tid] = make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+                    for (int b2 = 0; b2 < 3; ++b2)
+                        words[b2 * 4] |= (((code15[0] >> b2) & 1u) << 15) | (((code15[1] >> b2) & 1u) << 31);
                 }
-            }
-            // phase 2 (~0.3% of codes): the exact fp64 code replaces the fast
-            // one. A rolled loop over the flagged codes (one copy of the fp64
-            // sequence keeps the kernel small); registers are selected, not
-            // indexed, so nothing goes to local memory.
-            while (slow) {
-                const int e = __ffs(slow) - 1;
-                slow &= slow - 1;
-                // the slice is in this thread's shared-memory slot (ragged
-                // slices were copied there above): no dynamically indexed
-                // register array, so nothing goes to local memory
-                const uint16_t* sb = reinterpret_cast<const uint16_t*>(&buf[cur][e >> 3][tid]);
-                const float x = __uint_as_float(static_cast<uint32_t>(sb[e & 7]) << 16);
-                const uint32_t ex = kMagicBits + static_cast<uint32_t>(
-                                                     quant_code_exact(x, gg.step, gg.zero, gg.lo, gg.hi));
-                if (BITS == 3 && ((e >> 1) & 15) == 15) {
-                    const uint32_t c = ex - kMagicBits + static_cast<uint32_t>(off);
-                    code15[0] = (e & 1) ? code15[0] : c;
-                    code15[1] = (e & 1) ? c : code15[1];
+                if constexpr (BITS == 4) {
+                    *reinterpret_cast<uint4*>(tbase + sl * 2048) = make_uint4(words[0], words[1], words[2], words[3]);
+                } else if constexpr (BITS == 8) {
+                    *reinterpret_cast<uint4*>(tbase + (2 * sl) * 2048) = make_uint4(words[0], words[1], words[2], words[3]);
+                    *reinterpret_cast<uint4*>(tbase + (2 * sl + 1) * 2048) = make_uint4(words[4], words[5], words[6], words[7]);
                 } else {
-                    const code_pos cp = locate_code(BITS, e);
-                    const int wi = cp.chunk * 4 + cp.word;
-                    const uint32_t delta = (ex - fast_bits(x)) << cp.shift;
 #pragma unroll
-                    for (int i = 0; i < SP::NW; ++i) words[i] += (i == wi) ? delta : 0u;
+                    for (int b2 = 0; b2 < 3; ++b2) *reinterpret_cast<uint32_t*>(tbase + b2 * 2048 + sl * 4) = words[b2 * 4];
                 }
-            }
-            if constexpr (BITS == 3) {
-                // pair 15: bit b of code 30 at bit 15, of code 31 at bit 31, of chunk b
-#pragma unroll
-                for (int b2 = 0; b2 < 3; ++b2)
-                    words[b2 * 4] |= (((code15[0] >> b2) & 1u) << 15) | (((code15[1] >> b2) & 1u) << 31);
-            }
-            if constexpr (BITS == 4) {
-                *reinterpret_cast<uint4*>(tbase + sl * 2048) = make_uint4(words[0], words[1], words[2], words[3]);
-            } else if constexpr (BITS == 8) {
-                *reinterpret_cast<uint4*>(tbase + (2 * sl) * 2048) = make_uint4(words[0], words[1], words[2], words[3]);
-                *reinterpret_cast<uint4*>(tbase + (2 * sl + 1) * 2048) = make_uint4(words[4], words[5], words[6], words[7]);
-            } else {
-#pragma unroll
-                for (int b2 = 0; b2 < 3; ++b2) *reinterpret_cast<uint32_t*>(tbase + b2 * 2048 + sl * 4) = words[b2 * 4];
             }
         }
     }
@@ -501,21 +490,37 @@ cudaError_t launch_quant_pack(const void* w, int64_t n_out, int64_t k_in,
                               double* zero64, cudaStream_t st) {
     const int G = static_cast<int>(ceil_div64(k_in, 128));
     // rows up to the 128-row tile boundary: padding rows get code 0 / scale 0
-    const int64_t items = ceil_div64(n_out, 128) * (128 / kQRows) * G;
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t items = ceil_div64(n_out, kQRows) * G;
+    if (n_out >= (int64_t(1) << 31) || k_in >= (int64_t(1) << 31) || items >= (int64_t(1) << 31))
+        return cudaErrorInvalidValue;  // 32-bit row / k / item cursors
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // the dynamic shared-memory opt-in is per device and per kernel
+    static std::atomic<unsigned> attr_done[64];
+    const unsigned bitmask = 1u << (bits == 3 ? 0 : bits == 4 ? 1 : bits == 8 ? 2 : 3);
+    if (dev < 0 || dev >= 64 || !(attr_done[dev].load(std::memory_order_acquire) & bitmask)) {
+        cudaError_t e = cudaSuccess;
+        switch (bits) {
+            case 3: e = cudaFuncSetAttribute(quant_pack_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kK1Smem)); break;
+            case 4: e = cudaFuncSetAttribute(quant_pack_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kK1Smem)); break;
+            case 8: e = cudaFuncSetAttribute(quant_pack_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kK1Smem)); break;
+            case 16: e = cudaFuncSetAttribute(quant_pack_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kK1Smem)); break;
+            default: return cudaErrorInvalidValue;
+        }
+        if (e != cudaSuccess) return e;
+        if (dev >= 0 && dev < 64) attr_done[dev].fetch_or(bitmask, std::memory_order_acq_rel);
     }
     const unsigned grid = static_cast<unsigned>(items < int64_t(HP_K1_CTAS) * sms ? items : int64_t(HP_K1_CTAS) * sms);
     auto* wp = static_cast<const __nv_bfloat16*>(w);
     auto* pp = static_cast<uint8_t*>(packed);
+    const int n = static_cast<int>(n_out), k = static_cast<int>(k_in), its = static_cast<int>(items);
     switch (bits) {
-        case 3: quant_pack_kernel<3><<<grid, 256, 0, st>>>(wp, n_out, k_in, ldw, G, sym, items, pp, scale, zero, step64, zero64); break;
-        case 4: quant_pack_kernel<4><<<grid, 256, 0, st>>>(wp, n_out, k_in, ldw, G, sym, items, pp, scale, zero, step64, zero64); break;
-        case 8: quant_pack_kernel<8><<<grid, 256, 0, st>>>(wp, n_out, k_in, ldw, G, sym, items, pp, scale, zero, step64, zero64); break;
-        case 16: quant_pack_kernel<16><<<grid, 256, 0, st>>>(wp, n_out, k_in, ldw, G, sym, items, pp, scale, zero, step64, zero64); break;
+        case 3: quant_pack_kernel<3><<<grid, 256, kK1Smem, st>>>(wp, n, k, ldw, G, sym, its, pp, scale, zero, step64, zero64); break;
+        case 4: quant_pack_kernel<4><<<grid, 256, kK1Smem, st>>>(wp, n, k, ldw, G, sym, its, pp, scale, zero, step64, zero64); break;
+        case 8: quant_pack_kernel<8><<<grid, 256, kK1Smem, st>>>(wp, n, k, ldw, G, sym, its, pp, scale, zero, step64, zero64); break;
+        case 16: quant_pack_kernel<16><<<grid, 256, kK1Smem, st>>>(wp, n, k, ldw, G, sym, its, pp, scale, zero, step64, zero64); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
