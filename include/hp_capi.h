@@ -101,6 +101,18 @@ hp_status hp_quant_pack(const void* w, int64_t n_out, int64_t k_in,
                         void* packed, float* scale, float* zero,
                         double* step64, double* zero64, hp_stream stream);
 
+/* K1 with K2's weight reduction fused: hp_quant_pack,
+ * plus the op's indicator weight statistics from the same pass over W:
+ * stats5[0] = d_w = n_out·k_in, [1] = w_min, [2] = w_max (exact; the
+ * layout of hp_indicator_stats). stats5 is a DEVICE pointer (5 doubles);
+ * [3..4] are not touched — hp_indicator_stats(w = NULL, x, ...) fills
+ * them without re-reading W.                                               */
+hp_status hp_quant_pack_stats(const void* w, int64_t n_out, int64_t k_in,
+                              int64_t ldw, int bits, int scheme, int rounding,
+                              void* packed, float* scale, float* zero,
+                              double* step64, double* zero64, double* stats5,
+                              hp_stream stream);
+
 /* Unpack (parity/inspection): stored codes as u8 [n_out × k_in] row-major
  * (symmetric codes carry the +hi offset, hi = 2^(bits-1)-1), and fp32
  * scale/zero [n_out × groups] row-major. For bits==16, `codes` receives the
@@ -118,7 +130,9 @@ hp_status hp_dequant(const hp_qweight* w, void* w_bf16, hp_stream stream);
  *   stats5[0] = d_w = n_out·k_in, [1] = w_min, [2] = w_max (exact),
  *   [3] = x_mean, [4] = x_var (population, fp64 accumulation) over all
  *   tokens·k_in elements of the calibration input x [tokens × ldx] bf16.
- * stats5 is a DEVICE pointer (5 doubles). x may be NULL (x stats = 0).   */
+ * stats5 is a DEVICE pointer (5 doubles). x may be NULL (x stats = 0).
+ * w may be NULL (then n_out/ldw are ignored and stats5[0..2] are left as
+ * they are: the weight part of hp_quant_pack_stats).                     */
 hp_status hp_indicator_stats(const void* w, int64_t n_out, int64_t k_in,
                              int64_t ldw, const void* x, int64_t tokens,
                              int64_t ldx, double* stats5, hp_stream stream);

@@ -91,6 +91,7 @@ def _load() -> C.CDLL:
         "hp_packed_bytes": (i64, [i64, i64, i32]),
         "hp_scale_count": (i64, [i64, i64]),
         "hp_quant_pack": (i32, [v, i64, i64, i64, i32, i32, i32, v, v, v, v, v, v]),
+        "hp_quant_pack_stats": (i32, [v, i64, i64, i64, i32, i32, i32, v, v, v, v, v, v, v]),
         "hp_quant_unpack": (i32, [P(hp_qweight), v, v, v, v]),
         "hp_dequant": (i32, [P(hp_qweight), v, v]),
         "hp_indicator_stats": (i32, [v, i64, i64, i64, v, i64, i64, v, v]),
@@ -151,7 +152,7 @@ lib = _load()
 
 EXPORTED = [
     "hp_last_error", "hp_abi_version", "hp_device_ok", "hp_packed_bytes", "hp_scale_count",
-    "hp_quant_pack", "hp_quant_unpack", "hp_dequant", "hp_indicator_stats",
+    "hp_quant_pack", "hp_quant_pack_stats", "hp_quant_unpack", "hp_dequant", "hp_indicator_stats",
     "hp_qlinear_workspace_bytes", "hp_qlinear", "hp_host_scaling_factor", "hp_host_g_of_x",
     "hp_host_indicator_csv", "hp_host_omega_from_stats", "hp_host_mc_output_variance", "hp_host_memcost", "hp_host_preset",
     "hp_host_make_schedule", "hp_host_simulate", "hp_host_plan_check", "hp_host_unit_order", "hp_host_latency_fit", "hp_host_latency_predict", "hp_set_sm_budget", "hp_set_pdl",

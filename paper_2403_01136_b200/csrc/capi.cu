@@ -22,7 +22,7 @@ extern int g_pdl;
 extern unsigned long long* g_trace;
 cudaError_t launch_quant_pack(const void* w, int64_t n_out, int64_t k_in, int64_t ldw,
                               int bits, int sym, void* packed, float* scale, float* zero,
-                              double* step64, double* zero64, cudaStream_t st);
+                              double* step64, double* zero64, double* stats5, cudaStream_t st);
 cudaError_t launch_unpack(const void* packed, const float* scale, const float* zero,
                           int64_t n_out, int64_t k_in, int bits, void* codes,
                           float* scale_rm, float* zero_rm, cudaStream_t st);
@@ -196,27 +196,45 @@ int64_t hp_scale_count(int64_t n_out, int64_t k_in) {
     return hp::ceil_div64(n_out, 128) * hp::ceil_div64(k_in, 128) * 128;
 }
 
+static hp_status quant_pack_impl(const char* who, const void* w, int64_t n_out, int64_t k_in,
+                                 int64_t ldw, int bits, int scheme, int rounding, void* packed,
+                                 float* scale, float* zero, double* step64, double* zero64,
+                                 double* stats5, hp_stream stream) {
+    if (!w || !packed) return fail(HP_EINVAL, std::string(who) + ": NULL w or packed");
+    if (n_out <= 0 || k_in <= 0) return fail(HP_EINVAL, std::string(who) + ": empty shape");
+    if (ldw < k_in) return fail(HP_EINVAL, std::string(who) + ": ldw < k_in");
+    if (!bits_ok(bits)) return fail(HP_EINVAL, std::string(who) + ": bits must be 3, 4, 8 or 16");
+    if (scheme != HP_ASYMMETRIC && scheme != HP_SYMMETRIC)
+        return fail(HP_EINVAL, std::string(who) + ": unknown scheme");
+    if (rounding != HP_NEAREST)
+        return fail(HP_EINVAL, std::string(who) +
+                                   ": only round-to-nearest is supported on the GPU (the "
+                                   "reference's stochastic rounding draws a sequential mt19937_64 stream)");
+    if (bits != 16 && !scale) return fail(HP_EINVAL, std::string(who) + ": scale is NULL");
+    if ((step64 == nullptr) != (zero64 == nullptr))
+        return fail(HP_EINVAL, std::string(who) + ": step64 and zero64 go together");
+    if (n_out >= (int64_t(1) << 31) || k_in >= (int64_t(1) << 31))
+        return fail(HP_EINVAL, std::string(who) + ": n_out and k_in must be < 2^31");
+    if (hp_status s = need_device()) return s;
+    return cuda_status(hp::launch_quant_pack(w, n_out, k_in, ldw, bits, scheme, packed, scale,
+                                             zero, step64, zero64, stats5,
+                                             static_cast<cudaStream_t>(stream)),
+                       who);
+}
+
 hp_status hp_quant_pack(const void* w, int64_t n_out, int64_t k_in, int64_t ldw, int bits,
                         int scheme, int rounding, void* packed, float* scale, float* zero,
                         double* step64, double* zero64, hp_stream stream) {
-    if (!w || !packed) return fail(HP_EINVAL, "quant_pack: NULL w or packed");
-    if (n_out <= 0 || k_in <= 0) return fail(HP_EINVAL, "quant_pack: empty shape");
-    if (ldw < k_in) return fail(HP_EINVAL, "quant_pack: ldw < k_in");
-    if (!bits_ok(bits)) return fail(HP_EINVAL, "quant_pack: bits must be 3, 4, 8 or 16");
-    if (scheme != HP_ASYMMETRIC && scheme != HP_SYMMETRIC)
-        return fail(HP_EINVAL, "quant_pack: unknown scheme");
-    if (rounding != HP_NEAREST)
-        return fail(HP_EINVAL,
-                    "quant_pack: only round-to-nearest is supported on the GPU (the "
-                    "reference's stochastic rounding draws a sequential mt19937_64 stream)");
-    if (bits != 16 && !scale) return fail(HP_EINVAL, "quant_pack: scale is NULL");
-    if ((step64 == nullptr) != (zero64 == nullptr))
-        return fail(HP_EINVAL, "quant_pack: step64 and zero64 go together");
-    if (hp_status s = need_device()) return s;
-    return cuda_status(hp::launch_quant_pack(w, n_out, k_in, ldw, bits, scheme, packed, scale,
-                                             zero, step64, zero64,
-                                             static_cast<cudaStream_t>(stream)),
-                       "quant_pack");
+    return quant_pack_impl("quant_pack", w, n_out, k_in, ldw, bits, scheme, rounding, packed, scale,
+                           zero, step64, zero64, nullptr, stream);
+}
+
+hp_status hp_quant_pack_stats(const void* w, int64_t n_out, int64_t k_in, int64_t ldw, int bits,
+                              int scheme, int rounding, void* packed, float* scale, float* zero,
+                              double* step64, double* zero64, double* stats5, hp_stream stream) {
+    if (!stats5) return fail(HP_EINVAL, "quant_pack_stats: NULL stats5");
+    return quant_pack_impl("quant_pack_stats", w, n_out, k_in, ldw, bits, scheme, rounding, packed,
+                           scale, zero, step64, zero64, stats5, stream);
 }
 
 hp_status hp_quant_unpack(const hp_qweight* w, void* codes, float* scale_rm, float* zero_rm,
@@ -265,9 +283,10 @@ static cudaMemPool_t scratch_pool() {
 hp_status hp_indicator_stats(const void* w, int64_t n_out, int64_t k_in, int64_t ldw,
                              const void* x, int64_t tokens, int64_t ldx, double* stats5,
                              hp_stream stream) {
-    if (!w || !stats5) return fail(HP_EINVAL, "indicator_stats: NULL w or stats5");
-    if (n_out <= 0 || k_in <= 0) return fail(HP_EINVAL, "indicator_stats: empty weight");
-    if (ldw < k_in) return fail(HP_EINVAL, "indicator_stats: ldw < k_in");
+    if (!stats5) return fail(HP_EINVAL, "indicator_stats: NULL stats5");
+    if (!w && !x) return fail(HP_EINVAL, "indicator_stats: NULL w and x");
+    if (k_in <= 0) return fail(HP_EINVAL, "indicator_stats: empty k_in");
+    if (w && (n_out <= 0 || ldw < k_in)) return fail(HP_EINVAL, "indicator_stats: bad weight shape");
     if (x && (tokens <= 0 || ldx < k_in))
         return fail(HP_EINVAL, "indicator_stats: bad calibration shape");
     if (hp_status s = need_device()) return s;
@@ -281,10 +300,12 @@ hp_status hp_indicator_stats(const void* w, int64_t n_out, int64_t k_in, int64_t
     }
     // (an X element costs ~4x a W element: fp64 moments vs fp32 min/max, so
     // X blocks get proportionally fewer bytes and finish with the W blocks)
-    const double wb = static_cast<double>(n_out) * k_in, xb = x ? 4.0 * tokens * k_in : 0.0;
+    // w == NULL: the weight part was produced by hp_quant_pack_stats (K1's
+    // fused pass); only stats5[3..4] are written
+    const double wb = w ? static_cast<double>(n_out) * k_in : 0.0, xb = x ? 4.0 * tokens * k_in : 0.0;
     const int nb = 3 * sms;
-    const int nbx = x ? std::max(1, std::min(nb - 1, static_cast<int>(nb * xb / (wb + xb)))) : 0;
-    const int nbw = std::max(1, nb - nbx);
+    const int nbx = !x ? 0 : (!w ? nb : std::max(1, std::min(nb - 1, static_cast<int>(nb * xb / (wb + xb)))));
+    const int nbw = !w ? 0 : std::max(1, nb - nbx);
     const size_t bytes = hp::stats_scratch_bytes(nbw, nbx);
     void* scratch = nullptr;
     // stream-ordered scratch from a private pool that keeps its memory: a

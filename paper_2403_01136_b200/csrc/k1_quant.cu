@@ -116,6 +116,14 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// float <-> int with the same total order (negative floats: magnitude bits
+// flipped), for atomicMin / atomicMax on float values
+__device__ __forceinline__ int ordered_bits(float f) {
+    const int i = __float_as_int(f);
+    return i >= 0 ? i : i ^ 0x7fffffff;
+}
+__device__ __forceinline__ float from_ordered_bits(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); }
+
 __device__ __forceinline__ uint64_t splat2(float f) {
     const uint64_t b = __float_as_uint(f);
     return b | (b << 32);
@@ -181,8 +189,13 @@ __global__ void __launch_bounds__(256, HP_K1_CTAS)
     quant_pack_kernel(const __nv_bfloat16* __restrict__ w, int n_out, int k_in, int64_t ldw,
                       int G, int sym, int items, uint8_t* __restrict__ packed,
                       float* __restrict__ scale, float* __restrict__ zero,
-                      double* __restrict__ step64, double* __restrict__ zero64) {
+                      double* __restrict__ step64, double* __restrict__ zero64,
+                      int* __restrict__ wmm) {
     extern __shared__ __align__(16) uint4 kbuf[];  // [stage][piece][thread]
+    // K2's weight reduction fused into this pass: the
+    // op's exact min / max over all real weights, folded per thread and
+    // published once per warp (order-independent, so deterministic)
+    float tmin = __int_as_float(0x7f800000), tmax = -__int_as_float(0x7f800000);
     const int tid = threadIdx.x;
     const int h = tid & 1;     // k half of the group: slices 2h, 2h+1
     const int rin = tid >> 1;  // row within the 128-row block
@@ -253,6 +266,15 @@ __global__ void __launch_bounds__(256, HP_K1_CTAS)
 #pragma unroll
             for (int c = 0; c < kPieces; ++c)
                 *reinterpret_cast<uint4*>(tbase + (8 * h + c) * 2048) = *slot(cur, c);
+            if (wmm) {
+                for (int e = 0; e < valid; ++e) {
+                    const float x = __uint_as_float(static_cast<uint32_t>(
+                                                        reinterpret_cast<const uint16_t*>(slot(cur, e >> 3))[e & 7])
+                                                    << 16);
+                    tmin = fminf(tmin, x);
+                    tmax = fmaxf(tmax, x);
+                }
+            }
             continue;
         } else {
             // the thread's 64 elements, read from shared memory once
@@ -287,6 +309,10 @@ __global__ void __launch_bounds__(256, HP_K1_CTAS)
             wmin = fminf(wmin, __shfl_xor_sync(0xffffffffu, wmin, 1));
             wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, 1));
             if (!row_ok) wmin = wmax = 0.0f;
+            else if (wmm) {
+                tmin = fminf(tmin, wmin);
+                tmax = fmaxf(tmax, wmax);
+            }
             const group_grid gg = make_grid(wmin, wmax, BITS, sym != 0);
             const int off = sym ? (1 << (BITS - 1)) - 1 : 0;
             if (h == 0) {
@@ -403,6 +429,31 @@ __global__ void __launch_bounds__(256, HP_K1_CTAS)
         }
     }
     cp_async_wait<0>();
+    if (wmm) {
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            tmin = fminf(tmin, __shfl_xor_sync(0xffffffffu, tmin, d));
+            tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, d));
+        }
+        if ((tid & 31) == 0) {
+            atomicMin(&wmm[0], ordered_bits(tmin));
+            atomicMax(&wmm[1], ordered_bits(tmax));
+        }
+    }
+}
+
+// weight min/max scratch (two ordered ints in the bytes of stats5[1]) and
+// the fp64 result: stats5[0] = d_w, [1] = w_min, [2] = w_max (K2's layout)
+__global__ void wstats_init_kernel(int* wmm) {
+    wmm[0] = ordered_bits(__int_as_float(0x7f800000));
+    wmm[1] = ordered_bits(-__int_as_float(0x7f800000));
+}
+__global__ void wstats_finish_kernel(double* stats5, double d_w) {
+    const int* wmm = reinterpret_cast<const int*>(stats5 + 1);
+    const float mn = from_ordered_bits(wmm[0]), mx = from_ordered_bits(wmm[1]);
+    stats5[0] = d_w;
+    stats5[1] = static_cast<double>(mn);
+    stats5[2] = static_cast<double>(mx);
 }
 
 // Unpack to row-major stored codes (u8, or raw bf16 words for 16-bit) and
@@ -487,7 +538,7 @@ __global__ void dequant_kernel(const uint8_t* __restrict__ packed,
 cudaError_t launch_quant_pack(const void* w, int64_t n_out, int64_t k_in,
                               int64_t ldw, int bits, int sym, void* packed,
                               float* scale, float* zero, double* step64,
-                              double* zero64, cudaStream_t st) {
+                              double* zero64, double* stats5, cudaStream_t st) {
     const int G = static_cast<int>(ceil_div64(k_in, 128));
     // rows up to the 128-row tile boundary: padding rows get code 0 / scale 0
     const int64_t items = ceil_div64(n_out, kQRows) * G;
@@ -516,13 +567,16 @@ cudaError_t launch_quant_pack(const void* w, int64_t n_out, int64_t k_in,
     auto* wp = static_cast<const __nv_bfloat16*>(w);
     auto* pp = static_cast<uint8_t*>(packed);
     const int n = static_cast<int>(n_out), k = static_cast<int>(k_in), its = static_cast<int>(items);
+    int* wmm = stats5 ? reinterpret_cast<int*>(stats5 + 1) : nullptr;
+    if (wmm) wstats_init_kernel<<<1, 1, 0, st>>>(wmm);
     switch (bits) {
-        case 3: quant_pack_kernel<3><<<grid, 256, kK1Smem, st>>>(wp, n, k, ldw, G, sym, its, pp, scale, zero, step64, zero64); break;
-        case 4: quant_pack_kernel<4><<<grid, 256, kK1Smem, st>>>(wp, n, k, ldw, G, sym, its, pp, scale, zero, step64, zero64); break;
-        case 8: quant_pack_kernel<8><<<grid, 256, kK1Smem, st>>>(wp, n, k, ldw, G, sym, its, pp, scale, zero, step64, zero64); break;
-        case 16: quant_pack_kernel<16><<<grid, 256, kK1Smem, st>>>(wp, n, k, ldw, G, sym, its, pp, scale, zero, step64, zero64); break;
+        case 3: quant_pack_kernel<3><<<grid, 256, kK1Smem, st>>>(wp, n, k, ldw, G, sym, its, pp, scale, zero, step64, zero64, wmm); break;
+        case 4: quant_pack_kernel<4><<<grid, 256, kK1Smem, st>>>(wp, n, k, ldw, G, sym, its, pp, scale, zero, step64, zero64, wmm); break;
+        case 8: quant_pack_kernel<8><<<grid, 256, kK1Smem, st>>>(wp, n, k, ldw, G, sym, its, pp, scale, zero, step64, zero64, wmm); break;
+        case 16: quant_pack_kernel<16><<<grid, 256, kK1Smem, st>>>(wp, n, k, ldw, G, sym, its, pp, scale, zero, step64, zero64, wmm); break;
         default: return cudaErrorInvalidValue;
     }
+    if (wmm) wstats_finish_kernel<<<1, 1, 0, st>>>(stats5, static_cast<double>(n_out) * static_cast<double>(k_in));
     return cudaGetLastError();
 }
 

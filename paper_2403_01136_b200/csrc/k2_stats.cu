@@ -191,9 +191,11 @@ __global__ void __launch_bounds__(kStatThreads, 3)
     __syncthreads();
     xr = block_fold(xr, mg, sx);
     if (tid != 0) return;
-    out[0] = static_cast<double>(n_out) * static_cast<double>(k_in);
-    out[1] = static_cast<double>(wr.x);
-    out[2] = static_cast<double>(wr.y);
+    if (nbw > 0) {  // nbw == 0: the weight part came from K1's fused pass
+        out[0] = static_cast<double>(n_out) * static_cast<double>(k_in);
+        out[1] = static_cast<double>(wr.x);
+        out[2] = static_cast<double>(wr.y);
+    }
     out[3] = xr.n > 0.0 ? xr.mean : 0.0;
     out[4] = xr.n > 0.0 ? xr.m2 / xr.n : 0.0;
     *ticket = 0u;  // self-resetting for the next call

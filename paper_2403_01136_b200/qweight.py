@@ -62,11 +62,13 @@ def packed_bytes(n_out: int, k_in: int, bits: int) -> int:
 
 def quantize(w: torch.Tensor, bits: int, scheme: int = capi.HP_SYMMETRIC,
              rounding: int = capi.HP_NEAREST, want_fp64: bool = False,
-             stream: torch.cuda.Stream | None = None):
+             stream: torch.cuda.Stream | None = None, stats: torch.Tensor | None = None):
     """K1: group-wise quantize + pack a bf16 [n_out, k_in] CUDA tensor.
 
     Returns QuantizedWeight, plus (step64, zero64) [n_out, G] fp64 tensors
     when want_fp64 is set (the reference's per-group step / grid origin).
+    stats: optional device fp64[5]; K1's pass also writes the indicator's
+    weight statistics into stats[0..2] (hp_quant_pack_stats).
     """
     assert w.dtype == torch.bfloat16 and w.is_cuda and w.dim() == 2
     n_out, k_in = w.shape
@@ -86,9 +88,15 @@ def quantize(w: torch.Tensor, bits: int, scheme: int = capi.HP_SYMMETRIC,
         G = -(-k_in // GROUP)
         step64 = torch.empty(n_out, G, dtype=torch.float64, device=dev)
         zero64 = torch.empty(n_out, G, dtype=torch.float64, device=dev)
-    check(lib.hp_quant_pack(w.data_ptr(), n_out, k_in, ldw, bits, scheme, rounding,
-                            packed.data_ptr(), _ptr(scale), _ptr(zero), _ptr(step64),
-                            _ptr(zero64), _stream(stream)))
+    if stats is not None:
+        assert stats.dtype == torch.float64 and stats.numel() >= 5 and stats.device == dev
+        check(lib.hp_quant_pack_stats(w.data_ptr(), n_out, k_in, ldw, bits, scheme, rounding,
+                                      packed.data_ptr(), _ptr(scale), _ptr(zero), _ptr(step64),
+                                      _ptr(zero64), stats.data_ptr(), _stream(stream)))
+    else:
+        check(lib.hp_quant_pack(w.data_ptr(), n_out, k_in, ldw, bits, scheme, rounding,
+                                packed.data_ptr(), _ptr(scale), _ptr(zero), _ptr(step64),
+                                _ptr(zero64), _stream(stream)))
     qw = QuantizedWeight(n_out, k_in, bits, scheme, packed, scale, zero)
     if want_fp64:
         return qw, step64, zero64
@@ -117,14 +125,21 @@ def dequant(qw: QuantizedWeight, stream=None) -> torch.Tensor:
     return out
 
 
-def indicator_stats(w: torch.Tensor, x: torch.Tensor | None, stream=None) -> torch.Tensor:
-    """K2: device fp64[5] = {d_w, w_min, w_max, x_mean, x_var}."""
-    n_out, k_in = w.shape
-    out = torch.empty(5, dtype=torch.float64, device=w.device)
+def indicator_stats(w: torch.Tensor | None, x: torch.Tensor | None, stream=None,
+                    out: torch.Tensor | None = None) -> torch.Tensor:
+    """K2: device fp64[5] = {d_w, w_min, w_max, x_mean, x_var}.
+
+    w=None: only the calibration part [3..4] is written into `out` (whose
+    [0..2] came from quantize(..., stats=out), K1's fused weight pass)."""
+    assert w is not None or (x is not None and out is not None)
+    n_out, k_in = w.shape if w is not None else (0, x.shape[1])
+    dev = (w if w is not None else x).device
+    if out is None:
+        out = torch.empty(5, dtype=torch.float64, device=dev)
     tokens = 0 if x is None else x.shape[0]
     ldx = 0 if x is None else x.stride(0)
-    check(lib.hp_indicator_stats(w.data_ptr(), n_out, k_in, w.stride(0), _ptr(x), tokens, ldx,
-                                 out.data_ptr(), _stream(stream)))
+    check(lib.hp_indicator_stats(_ptr(w), n_out, k_in, 0 if w is None else w.stride(0), _ptr(x),
+                                 tokens, ldx, out.data_ptr(), _stream(stream)))
     return out
 
 

@@ -69,6 +69,20 @@ def main():
                              "scheme": "sym" if scheme == capi.HP_SYMMETRIC else "asym",
                              "us": t * 1e6, "alg_bytes": by, "GBs": by / t / 1e9, "frac": by / t / 1e9 / hbm})
                 print(json.dumps(rows[-1]), flush=True)
+                if b == 4 and scheme == capi.HP_ASYMMETRIC:
+                    # K1 with K2's weight min/max fused (hp_quant_pack_stats)
+                    stt = torch.empty(5, dtype=torch.float64, device=dev)
+
+                    def k1s():
+                        capi.check(capi.lib.hp_quant_pack_stats(
+                            w.data_ptr(), n, k, k, b, scheme, capi.HP_NEAREST, qw.packed.data_ptr(),
+                            qw.scale.data_ptr(), qw.zero.data_ptr(), None, None, stt.data_ptr(),
+                            st.cuda_stream))
+                    t = timed(k1s)
+                    rows.append({"kernel": "K1+stats", "shape": [n, k], "bits": b, "scheme": "asym",
+                                 "us": t * 1e6, "alg_bytes": by, "GBs": by / t / 1e9,
+                                 "frac": by / t / 1e9 / hbm})
+                    print(json.dumps(rows[-1]), flush=True)
                 del qw
         x = (torch.randn(args.tokens, k, device=dev) + 0.05).to(torch.bfloat16)
         out = torch.empty(5, dtype=torch.float64, device=dev)
@@ -81,9 +95,18 @@ def main():
         rows.append({"kernel": "K2", "shape": [n, k], "tokens": args.tokens, "us": t * 1e6,
                      "alg_bytes": by, "GBs": by / t / 1e9, "frac": by / t / 1e9 / hbm})
         print(json.dumps(rows[-1]), flush=True)
+
+        def k2x():  # calibration part only: the weight part came from K1's fused pass
+            capi.check(capi.lib.hp_indicator_stats(None, 0, k, 0, x.data_ptr(), args.tokens, k,
+                                                   out.data_ptr(), st.cuda_stream))
+        t = timed(k2x)
+        by = args.tokens * k * 2
+        rows.append({"kernel": "K2 (x only)", "shape": [n, k], "tokens": args.tokens, "us": t * 1e6,
+                     "alg_bytes": by, "GBs": by / t / 1e9, "frac": by / t / 1e9 / hbm})
+        print(json.dumps(rows[-1]), flush=True)
     print(json.dumps({"summary": True, "hbm_gbs": hbm,
                       "k1_best_frac": max(r["frac"] for r in rows if r["kernel"] == "K1"),
-                      "k2_best_frac": max(r["frac"] for r in rows if r["kernel"] == "K2")}))
+                      "k2_best_frac": max(r["frac"] for r in rows if r["kernel"] == "K2")}))  # noqa: E501
 
 
 if __name__ == "__main__":
