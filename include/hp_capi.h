@@ -159,8 +159,9 @@ hp_status hp_layernorm(const void* x, int64_t ldx, int64_t rows, int64_t h, cons
 
 /* Decoder glue (decoder.cu), device pointers, bf16
  * unless noted. qkv rows are [q | k | v] (h columns each, head hd-column
- * blocks); hd = 64 or 128. The K/V cache of a layer is [B][S_max][h] for K
- * then V (memcost.cpp:38-42).
+ * blocks); hd = 64 or 128. The K/V cache of a layer is head-major
+ * [B][h/hd][S_max][hd] for K and for V (the 2*v*(s+n)*h1 elements of
+ * memcost.cpp:38-42; one (request, head) context is contiguous).
  *  hp_embed: x[r] = E[tok[r]] + P[pos(r) + 2] (OPT learned positions;
  *    pos(r) = pos0 + r % s_tokens if pos_per_req else pos0; P may be NULL).
  *  hp_attention_prefill: causal self-attention of `reqs` requests of s

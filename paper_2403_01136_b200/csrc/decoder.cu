@@ -127,8 +127,10 @@ __device__ __forceinline__ uint32_t tile_off(int row, int chunk) {
 // ---------------------------------------------------------- prefill attention
 // grid (q-tiles of 16*NW, heads, requests); NW warps x 16 query rows.
 // qkv [rows x 3h] bf16 (request r's tokens at rows r*s .. r*s+s-1 of this
-// micro-batch); out [rows x h]; K/V cache rows of request (req0 + r) at
-// positions 0..s-1: cache + ((req0+r)*S_max + pos)*h.
+// micro-batch); out [rows x h]; K/V cache: head-major [B][heads][S_max][D],
+// request (req0 + r), head hd, position pos at ((req*heads + hd)*S_max + pos)*D
+// (the 2*v*(s+n)*h1 elements per layer of memcost.cpp:38-42, laid out so a
+// (request, head) context is ONE contiguous stream for decode attention).
 template <int D, int NW>
 __global__ void __launch_bounds__(32 * NW)
     attn_prefill_kernel(const __nv_bfloat16* __restrict__ qkv, int s, int h, float scale_log2,
@@ -155,7 +157,7 @@ __global__ void __launch_bounds__(32 * NW)
         cp_async16(smem_addr(sQ) + tile_off<D>(row, c), base + static_cast<int64_t>(q0 + row) * ld + c * 8,
                    ok);
         if (ok) {
-            const int64_t crow = (static_cast<int64_t>(req0 + r) * S_max + q0 + row) * h + head * D + c * 8;
+            const int64_t crow = ((static_cast<int64_t>(req0 + r) * (h / D) + head) * S_max + q0 + row) * D + c * 8;
             *reinterpret_cast<uint4*>(kc + crow) =
                 *reinterpret_cast<const uint4*>(base + static_cast<int64_t>(q0 + row) * ld + h + c * 8);
             *reinterpret_cast<uint4*>(vc + crow) =
@@ -326,15 +328,16 @@ __global__ void __launch_bounds__(128)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t ld = 3LL * h;
     const __nv_bfloat16* row = qkv + static_cast<int64_t>(r) * ld + head * D;
-    const int64_t cbase = static_cast<int64_t>(req0 + r) * S_max * h + head * D;
+    // head-major cache: this (request, head)'s keys are contiguous D-element rows
+    const int64_t cbase = (static_cast<int64_t>(req0 + r) * (h / D) + head) * S_max * D;
     float q[EL];
 #pragma unroll
     for (int e = 0; e < EL; ++e) q[e] = __bfloat162float(row[lane * EL + e]) * scale_log2;
     if (warp == 0 && z == nz - 1) {  // append k/v at p (the split that reads row p)
 #pragma unroll
         for (int e = 0; e < EL; ++e) {
-            kc[cbase + static_cast<int64_t>(p) * h + lane * EL + e] = row[h + lane * EL + e];
-            vc[cbase + static_cast<int64_t>(p) * h + lane * EL + e] = row[2 * h + lane * EL + e];
+            kc[cbase + static_cast<int64_t>(p) * D + lane * EL + e] = row[h + lane * EL + e];
+            vc[cbase + static_cast<int64_t>(p) * D + lane * EL + e] = row[2 * h + lane * EL + e];
         }
     }
     __syncthreads();  // the new row is visible to the CTA (same-CTA global RAW)
@@ -359,8 +362,8 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
         for (int u = 0; u < KU; ++u) {
             const int key = k0 + u < nk ? k0 + u : nk - 1;  // clamp: loads stay in bounds
-            kr[u] = *reinterpret_cast<const raw_t*>(kc + cbase + static_cast<int64_t>(key) * h + lane * EL);
-            vr[u] = *reinterpret_cast<const raw_t*>(vc + cbase + static_cast<int64_t>(key) * h + lane * EL);
+            kr[u] = *reinterpret_cast<const raw_t*>(kc + cbase + static_cast<int64_t>(key) * D + lane * EL);
+            vr[u] = *reinterpret_cast<const raw_t*>(vc + cbase + static_cast<int64_t>(key) * D + lane * EL);
         }
         float sc[KU];
 #pragma unroll
@@ -550,28 +553,31 @@ cudaError_t launch_attn_prefill(const void* qkv, int reqs, int s, int h, int D, 
     return launch_ex(fn, grid, dim3(32 * kPrefillWarps), smem, st, args);
 }
 
-// Split-context scratch for launch_attn_decode: fp32 (M, L, acc[D]) per
-// (row, head, split) + a self-resetting ticket per (row, head); zero once.
+// Split-context scratch for launch_attn_decode: a FIXED-size region of
+// self-resetting tickets (one per (row, head) pair) at offset 0, then fp32
+// (M, L, acc[D]) per (row, head, split). Zero once. The ticket region does
+// not move with the configuration, so one workspace serves calls of any
+// (rows, heads, split): a per-configuration offset would put one call's
+// tickets over another call's (never re-zeroed) partials.
+constexpr size_t kAttnTicketPairs = size_t(1) << 17;
 size_t attn_decode_workspace(int rows, int h, int D, int split) {
     if (split <= 1) return 0;
     const size_t pairs = static_cast<size_t>(rows) * (h / D);
-    return pairs * split * (D + 2) * sizeof(float) + pairs * sizeof(unsigned);
+    return kAttnTicketPairs * sizeof(unsigned) + pairs * split * (D + 2) * sizeof(float);
 }
 
 cudaError_t launch_attn_decode(const void* qkv, int rows, int h, int D, int p, void* out, void* kc,
                                void* vc, int req0, int S_max, cudaStream_t st, void* ws, int split) {
-    if (p + 1 > 1024) return cudaErrorInvalidValue;  // s_sc holds the row's scores
+    if (split > 1 && static_cast<size_t>(rows) * (h / D) > kAttnTicketPairs) return cudaErrorInvalidValue;
     const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(D));
     const __nv_bfloat16* q = static_cast<const __nv_bfloat16*>(qkv);
     __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out);
     __nv_bfloat16* k = static_cast<__nv_bfloat16*>(kc);
     __nv_bfloat16* v = static_cast<__nv_bfloat16*>(vc);
     if (split < 1 || (split > 1 && !ws)) split = 1;
-    float* part = static_cast<float*>(ws);
-    unsigned* tick = split > 1 ? reinterpret_cast<unsigned*>(
-                                     static_cast<char*>(ws) +
-                                     static_cast<size_t>(rows) * (h / D) * split * (D + 2) * sizeof(float))
-                               : nullptr;
+    unsigned* tick = split > 1 ? static_cast<unsigned*>(ws) : nullptr;
+    float* part = split > 1 ? reinterpret_cast<float*>(static_cast<char*>(ws) + kAttnTicketPairs * sizeof(unsigned))
+                            : nullptr;
     void* args[] = {&q, &h, &p, const_cast<float*>(&scale_log2), &o, &k, &v, &req0, &S_max, &part, &tick};
     const dim3 grid(h / D, rows, split);
     if (D == 128) return launch_ex(reinterpret_cast<const void*>(attn_decode_kernel<128>), grid, dim3(128), 0, st, args);

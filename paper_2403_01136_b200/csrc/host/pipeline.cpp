@@ -319,8 +319,11 @@ struct pipeline::impl {
     std::vector<void*> dec_x;    // per group [xi_g x h1]
     void* ws = nullptr;
     size_t ws_bytes = 0;
-    // decode attention: context split over 2 CTAs per (request, head)
-    static constexpr int kAttnSplit = 2;
+    // decode attention: the context is split over attn_split CTAs per
+    // (request, head) only when the (request, head) pairs alone would not
+    // fill the SMs (~8 resident CTAs each); with the head-major cache one
+    // CTA per pair streams contiguous rows at ~0.92 of HBM
+    int attn_split = 1;
     void* attn_ws = nullptr;
     int64_t weight_bytes = 0;
     load_stats lstats;
@@ -593,7 +596,16 @@ struct pipeline::impl {
             ws = alloc(ws_bytes);
             cuda_ok(cudaMemsetAsync(ws, 0, ws_bytes, cs), "ws");
         }
-        if (const size_t ab = hp::attn_decode_workspace(xi, static_cast<int>(h1), hd, kAttnSplit)) {
+        {
+            int dev = 0, sms = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            int min_pairs = xi;  // the smallest decode group
+            for (int gs : group_size) min_pairs = std::min(min_pairs, gs);
+            min_pairs *= static_cast<int>(h1 / hd);
+            attn_split = std::max(1, std::min(8, (8 * sms + min_pairs - 1) / std::max(1, min_pairs)));
+        }
+        if (const size_t ab = hp::attn_decode_workspace(xi, static_cast<int>(h1), hd, attn_split)) {
             attn_ws = alloc(ab);
             cuda_ok(cudaMemsetAsync(attn_ws, 0, ab, cs), "attention ws");
         }
@@ -686,7 +698,7 @@ struct pipeline::impl {
             } else {
                 cuda_ok(hp::launch_attn_decode(scr_qkv, u.nreq, static_cast<int>(h1), hd, u.pos, scr_a,
                                                kcache(L), vcache(L), u.req0, S_max, cs, attn_ws,
-                                               kAttnSplit),
+                                               attn_split),
                         "attention (decode)");
             }
             record(ev, 8);

@@ -1,7 +1,8 @@
 """Decoder glue kernels (csrc/decoder.cu) against plain
 torch fp32 references: causal prefill attention writing the KV cache,
-decode attention over the cache (memcost.cpp:38-42 layout [B][S_max][h]),
-token + position embedding (OPT, offset 2) and greedy argmax."""
+decode attention over the cache (memcost.cpp:38-42 sizes; head-major
+layout [B][heads][S_max][hd]), token + position embedding (OPT, offset 2)
+and greedy argmax."""
 import math
 
 import pytest
@@ -31,11 +32,12 @@ def test_prefill_attention_and_cache_write(cuda, hd, heads, s):
     g = torch.Generator(device=cuda).manual_seed(hd + s)
     h, reqs, B, S_max = heads * hd, 3, 5, s + 40
     qkv = torch.randn(reqs * s, 3 * h, generator=g, device=cuda).to(torch.bfloat16)
-    kc = torch.zeros(B, S_max, h, dtype=torch.bfloat16, device=cuda)
+    kc = torch.zeros(B, heads, S_max, hd, dtype=torch.bfloat16, device=cuda)
     vc = torch.zeros_like(kc)
     req0 = 1
     out = qweight.attention_prefill(qkv, reqs, s, hd, kc, vc, req0, S_max)
     torch.cuda.synchronize()
+    kc, vc = kc.transpose(1, 2).reshape(B, S_max, h), vc.transpose(1, 2).reshape(B, S_max, h)
     for r in range(reqs):
         rows = qkv[r * s:(r + 1) * s].float()
         q, k, v = (rows[:, i * h:(i + 1) * h].reshape(s, heads, hd) for i in range(3))
@@ -56,15 +58,17 @@ def test_decode_attention_appends_and_attends(cuda, hd, heads, p, split):
     from paper_2403_01136_b200 import qweight
     g = torch.Generator(device=cuda).manual_seed(hd * 7 + p)
     h, rows, B, S_max = heads * hd, 6, 9, 612
-    kc = torch.randn(B, S_max, h, generator=g, device=cuda).to(torch.bfloat16)
-    vc = torch.randn(B, S_max, h, generator=g, device=cuda).to(torch.bfloat16)
+    kh = torch.randn(B, heads, S_max, hd, generator=g, device=cuda).to(torch.bfloat16)
+    vh = torch.randn(B, heads, S_max, hd, generator=g, device=cuda).to(torch.bfloat16)
     qkv = torch.randn(rows, 3 * h, generator=g, device=cuda).to(torch.bfloat16)
     req0 = 2
-    k_before = kc.clone()
-    out = qweight.attention_decode(qkv, hd, p, kc, vc, req0, S_max, split=split)
+    k_before = kh.transpose(1, 2).reshape(B, S_max, h).clone()
+    out = qweight.attention_decode(qkv, hd, p, kh, vh, req0, S_max, split=split)
     torch.cuda.synchronize()
     if split > 1:  # deterministic merge of the splits: a rerun gives the same bits
-        assert torch.equal(out, qweight.attention_decode(qkv, hd, p, kc, vc, req0, S_max, split=split))
+        assert torch.equal(out, qweight.attention_decode(qkv, hd, p, kh, vh, req0, S_max, split=split))
+    # [B][S_max][h] views of the head-major caches for the checks below
+    kc, vc = kh.transpose(1, 2).reshape(B, S_max, h), vh.transpose(1, 2).reshape(B, S_max, h)
     for r in range(rows):
         assert torch.equal(kc[req0 + r, p], qkv[r, h:2 * h])
         assert torch.equal(vc[req0 + r, p], qkv[r, 2 * h:])

@@ -71,8 +71,15 @@ def main():
         kc = torch.randn(nreq, S_max, h1, device=dev).to(torch.bfloat16)
         vc = torch.randn(nreq, S_max, h1, device=dev).to(torch.bfloat16)
         stream = lambda: torch.cuda.current_stream().cuda_stream
-        # the executor's decode attention splits the context over 2 CTAs
-        aws_n = int(lib.hp_attention_decode_workspace_bytes(vmax_dec, h1, hd, 2))
+        # the executor's decode attention split (pipeline.cpp: one CTA per
+        # (request, head) unless the pairs would not fill ~8 CTAs per SM)
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+
+        def attn_split(v):
+            pairs = v * heads
+            return max(1, min(8, -(-8 * sms // pairs)))
+        aws_n = max(int(lib.hp_attention_decode_workspace_bytes(vmax_dec, h1, hd, attn_split(v)))
+                    for v in range(1, vmax_dec + 1))
         aws = torch.zeros(max(aws_n, 1), dtype=torch.uint8, device=dev)
 
         def stack(v, s, t, phase):
@@ -86,7 +93,7 @@ def main():
                                                    kc.data_ptr(), vc.data_ptr(), 0, S_max, stream()))
                 else:
                     check(lib.hp_attention_decode(qkv.data_ptr(), v, h1, hd, s + t - 1, a.data_ptr(),
-                                                  kc.data_ptr(), vc.data_ptr(), 0, S_max, 2,
+                                                  kc.data_ptr(), vc.data_ptr(), 0, S_max, attn_split(v),
                                                   aws.data_ptr(), aws_n, stream()))
                 qweight.qlinear(ops[1], a[:m], phase=phase, out=x[:m], residual=x[:m])
                 check(lib.hp_layernorm(x.data_ptr(), h1, m, h1, ln[2].data_ptr(), ln[3].data_ptr(),
