@@ -112,6 +112,90 @@ __global__ void __launch_bounds__(kThreads)
     }
 }
 
+// Decode-size LayerNorm (few rows, latency-bound inside the PDL chain of
+// the decode step): gamma / beta are staged in shared memory BEFORE
+// griddepcontrol.wait (they do not depend on the previous kernel), the row
+// is held as packed bf16 (4 registers per 8 elements), and the statistics
+// reduce over 128 threads. One CTA per row.
+template <int kVec>
+__global__ void __launch_bounds__(128)
+    layernorm_rows_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx, int h,
+                          const __nv_bfloat16* __restrict__ gamma, const __nv_bfloat16* __restrict__ beta,
+                          __nv_bfloat16* __restrict__ y, int64_t ldy) {
+    extern __shared__ uint4 gb[];  // [gamma | beta], h/8 vectors each
+    __shared__ float red[4];
+    const int nv = h >> 3;
+    for (int c = threadIdx.x; c < nv; c += 128) {
+        gb[c] = reinterpret_cast<const uint4*>(gamma)[c];
+        gb[nv + c] = reinterpret_cast<const uint4*>(beta)[c];
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const uint4* xr = reinterpret_cast<const uint4*>(x + blockIdx.x * ldx);
+    uint4* yr = reinterpret_cast<uint4*>(y + blockIdx.x * ldy);
+    uint4 q[kVec];
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) {
+        const int c = threadIdx.x + j * 128;
+        q[j] = c < nv ? xr[c] : make_uint4(0u, 0u, 0u, 0u);
+    }
+    auto block_sum = [&](float a) {
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) a += __shfl_xor_sync(0xffffffffu, a, d);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+        __syncthreads();
+        const float t = (red[0] + red[1]) + (red[2] + red[3]);
+        __syncthreads();
+        return t;
+    };
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) {
+        const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&q[j]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(p[e]);
+            s += f.x + f.y;
+        }
+    }
+    const float mean = block_sum(s) / static_cast<float>(h);
+    float v = 0.f;
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) {
+        if (threadIdx.x + j * 128 < nv) {
+            const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&q[j]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(p[e]);
+                v += (f.x - mean) * (f.x - mean) + (f.y - mean) * (f.y - mean);
+            }
+        }
+    }
+    const float rstd = rsqrtf(block_sum(v) / static_cast<float>(h) + 1e-5f);
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) {
+        const int c = threadIdx.x + j * 128;
+        if (c < nv) {
+            const uint4 gq = gb[c], bq = gb[nv + c];
+            const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&q[j]);
+            const __nv_bfloat162* gp = reinterpret_cast<const __nv_bfloat162*>(&gq);
+            const __nv_bfloat162* bp = reinterpret_cast<const __nv_bfloat162*>(&bq);
+            uint4 o;
+            uint32_t* op = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(p[e]);
+                const float2 gf = __bfloat1622float2(gp[e]);
+                const float2 bf = __bfloat1622float2(bp[e]);
+                const __nv_bfloat162 r = __floats2bfloat162_rn((f.x - mean) * rstd * gf.x + bf.x,
+                                                               (f.y - mean) * rstd * gf.y + bf.y);
+                op[e] = *reinterpret_cast<const uint32_t*>(&r);
+            }
+            yr[c] = o;
+        }
+    }
+}
+
 // dst[i] = src[(i * stride + offset)] rows of width h (bf16), i < rows
 __global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ src, int64_t lds,
                                    int64_t stride, int64_t offset, int rows, int h,
@@ -149,6 +233,26 @@ cudaError_t launch_layernorm(const void* x, int64_t ldx, int64_t rows, int h, co
     attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+#ifndef HP_LN_ROWS_MAX
+#define HP_LN_ROWS_MAX 256
+#endif
+    if (rows <= HP_LN_ROWS_MAX && h <= 8 * 128 * 16) {  // decode-size: the latency-bound variant
+        cfg.blockDim = dim3(128);
+        cfg.dynamicSmemBytes = static_cast<size_t>(h) * 4;  // gamma + beta
+        const auto* xp = static_cast<const __nv_bfloat16*>(x);
+        const auto* gp = static_cast<const __nv_bfloat16*>(gamma);
+        const auto* bp = static_cast<const __nv_bfloat16*>(beta);
+        auto* yp = static_cast<__nv_bfloat16*>(y);
+        const int nv = h / 8;
+        if (nv <= 128 * 4) return cudaLaunchKernelEx(&cfg, layernorm_rows_kernel<4>, xp, ldx, h, gp, bp, yp, ldy);
+        if (nv <= 128 * 8) return cudaLaunchKernelEx(&cfg, layernorm_rows_kernel<8>, xp, ldx, h, gp, bp, yp, ldy);
+        if (cfg.dynamicSmemBytes > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(layernorm_rows_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(cfg.dynamicSmemBytes));
+            if (e != cudaSuccess) return e;
+        }
+        return cudaLaunchKernelEx(&cfg, layernorm_rows_kernel<16>, xp, ldx, h, gp, bp, yp, ldy);
+    }
     return cudaLaunchKernelEx(&cfg, layernorm_kernel<256>, static_cast<const __nv_bfloat16*>(x), ldx,
                               h, static_cast<const __nv_bfloat16*>(gamma),
                               static_cast<const __nv_bfloat16*>(beta),

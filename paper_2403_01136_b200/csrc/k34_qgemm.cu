@@ -561,6 +561,13 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
             tc_commit_elect(&tfull[acc]);
             ++ut;
         }
+#ifdef HP_QGEMM_TRACE
+        if (lane == 0 && a.trace) {  // per-CTA: last MMA issued
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            a.trace[6 * kTraceIters * 4 + 4096 + blockIdx.x] = t;
+        }
+#endif
     } else if (warp >= 4 && warp < C::kEpiWarp0) {
         // ===================== dequant =====================
         const int q = warp - 4;
@@ -1069,8 +1076,8 @@ unsigned long long* trace_buffer() {
         if (getenv("HP_QGEMM_TRACE")) {
             int cta = getenv("HP_QGEMM_TRACE_CTA") ? atoi(getenv("HP_QGEMM_TRACE_CTA")) : 0;
             cudaMemcpyToSymbol(g_trace_cta, &cta, sizeof(int));
-            cudaMalloc(&g_trace, sizeof(unsigned long long) * (6 * kTraceIters * 4 + 4 * 1024));
-            cudaMemset(g_trace, 0, sizeof(unsigned long long) * (6 * kTraceIters * 4 + 4 * 1024));
+            cudaMalloc(&g_trace, sizeof(unsigned long long) * (6 * kTraceIters * 4 + 5 * 1024));
+            cudaMemset(g_trace, 0, sizeof(unsigned long long) * (6 * kTraceIters * 4 + 5 * 1024));
         }
     }
     return g_trace;

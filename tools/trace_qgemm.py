@@ -14,7 +14,8 @@ def main():
     from paper_2403_01136_b200 import qweight
     from paper_2403_01136_b200.capi import lib
     lib.hp_debug_trace.argtypes = [C.c_void_p, C.c_int]
-    n, k, bits, m = (int(v) for v in (sys.argv[1:] + ["20480", "5120", "4", "32"])[:4])
+    pos = [v for v in sys.argv[1:] if not v.startswith("--")]
+    n, k, bits, m = (int(v) for v in (pos + ["20480", "5120", "4", "32"][len(pos):])[:4])
     dev = torch.device("cuda:0")
     w = (torch.randn(n, k, device=dev) * 0.02).to(torch.bfloat16)
     qw = qweight.quantize(w, bits)
@@ -22,7 +23,7 @@ def main():
     for _ in range(3):
         qweight.qlinear(qw, x, phase=1)
     torch.cuda.synchronize()
-    buf = np.zeros(6 * 64 * 4 + 4 * 1024, dtype=np.uint64)
+    buf = np.zeros(6 * 64 * 4 + 5 * 1024, dtype=np.uint64)
     lib.hp_debug_trace(buf.ctypes.data, buf.size)
     cyc = buf[6 * 64 * 4 + 2048:6 * 64 * 4 + 2048 + 148].astype(np.int64)
     cta = buf[6 * 64 * 4:6 * 64 * 4 + 2048].reshape(1024, 2).astype(np.int64)
@@ -33,9 +34,20 @@ def main():
     print(f"CTAs {len(cta)}: entry min/med/max {ent.min():.2f}/{np.median(ent):.2f}/{ent.max():.2f} us; "
           f"exit min/med/max {ext.min():.2f}/{np.median(ext):.2f}/{ext.max():.2f} us")
     print("  exit sorted (last 10):", np.round(np.sort(ext)[-10:], 2), " argmax", int(np.argmax(ext)))
-    print("  exit by CTA:", " ".join(f"{v:.1f}" for v in ext))
+    if "--all" in sys.argv:
+        print("  exit by CTA:", " ".join(f"{v:.1f}" for v in ext))
     smid = buf[6 * 64 * 4 + 2048 + 1024:6 * 64 * 4 + 2048 + 1024 + 148].astype(np.int64)
-    print("  smid by CTA:", " ".join(str(v) for v in smid))
+    if "--all" in sys.argv:
+        print("  smid by CTA:", " ".join(str(v) for v in smid))
+    mend = buf[6 * 64 * 4 + 4096:6 * 64 * 4 + 4096 + len(cta)].astype(np.int64)
+    if mend.min() > 0:
+        me = (mend - t0c) / 1000
+        print(f"  last MMA issued min/med/max {me.min():.2f}/{np.median(me):.2f}/{me.max():.2f} us; "
+              f"exit - last MMA med/max {np.median(ext - me):.2f}/{(ext - me).max():.2f} us; "
+              f"slowest-MMA CTAs {np.argsort(me)[-5:].tolist()} on SMs "
+              f"{[int(smid[i]) for i in np.argsort(me)[-5:]]}")
+        if "--all" in sys.argv:
+            print("  last MMA by CTA:", " ".join(f"{v:.1f}" for v in me))
     span_ns = (cta[:148, 1] - cta[:148, 0]).astype(np.float64)
     print(f"  CTA cycles/ns (implied GHz): median {np.median(cyc / span_ns):.3f}, cycles median {np.median(cyc):.0f}")
     g = torch.cuda.CUDAGraph()
@@ -52,6 +64,8 @@ def main():
     print(f"  graph b2b per launch: {e0.elapsed_time(e1) * 100:.1f} us")
     t = buf[:6 * 64 * 4].reshape(6, 64, 4).astype(np.int64)
     t0 = t[t > 0].min()
+    if "--roles" not in sys.argv:
+        return
     names = ["producer (start, empty_ok, issued)", "mma (start, full_ok, afull_ok, committed)",
              "dequant w4 (start, full_ok, aempty_ok, arrived)", "epilogue seg (start, tfull_ok, stored, fixup_done) @48..",
              "dequant w4 detail (codes_loaded, st_issued, st_done, -)",
