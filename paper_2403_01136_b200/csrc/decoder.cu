@@ -124,6 +124,12 @@ __device__ __forceinline__ uint32_t tile_off(int row, int chunk) {
     return static_cast<uint32_t>((row * (D / 8) + (chunk ^ (row & 7))) * 16);
 }
 
+constexpr int kPrefillWarps = 4;
+#ifndef HP_ATTN_PRE_STAGES
+#define HP_ATTN_PRE_STAGES 2
+#endif
+constexpr int kPrefillStages = HP_ATTN_PRE_STAGES;  // K/V ring depth: 2 and 3 measure the same (107 TF/s), 4 (1 CTA/SM) 68
+
 // ---------------------------------------------------------- prefill attention
 // grid (q-tiles of 16*NW, heads, requests); NW warps x 16 query rows.
 // qkv [rows x 3h] bf16 (request r's tokens at rows r*s .. r*s+s-1 of this
@@ -138,13 +144,17 @@ __global__ void __launch_bounds__(32 * NW)
                         __nv_bfloat16* __restrict__ vc, int req0, int S_max) {
     constexpr int BR = 16 * NW, BC = 64, CH = D / 8;  // 16-byte chunks per row
     constexpr int NT = 32 * NW;
+    constexpr int KS = kPrefillStages;      // K/V tile ring depth
     extern __shared__ __align__(128) uint8_t sm[];
     uint8_t* sQ = sm;
-    uint8_t* sK = sm + BR * D * 2;          // 2 stages
-    uint8_t* sV = sK + 2 * BC * D * 2;      // 2 stages
+    uint8_t* sK = sm + BR * D * 2;          // KS stages
+    uint8_t* sV = sK + KS * BC * D * 2;     // KS stages
     pdl_wait_glue();
     pdl_trigger_glue();
-    const int qt = blockIdx.x, head = blockIdx.y, r = blockIdx.z;
+    // grid (heads, requests, q-tiles), the LAST (most key tiles under the
+    // causal mask) q-tiles first: the long CTAs start in the first wave and
+    // the short ones fill the tail
+    const int head = blockIdx.x, r = blockIdx.y, qt = gridDim.z - 1 - blockIdx.z;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t ld = 3LL * h;
     const __nv_bfloat16* base = qkv + static_cast<int64_t>(r) * s * ld + head * D;
@@ -167,6 +177,10 @@ __global__ void __launch_bounds__(32 * NW)
     cp_commit();
     const int nkv = (q0 + BR + BC - 1) / BC;  // causal: key tiles 0 .. q-tile
     auto load_kv = [&](int j, int stg) {
+        if (j >= nkv) {  // empty group: keeps the wait count uniform
+            cp_commit();
+            return;
+        }
         for (int i = tid; i < BC * CH; i += NT) {
             const int row = i / CH, c = i % CH;
             const int key = j * BC + row;
@@ -177,8 +191,9 @@ __global__ void __launch_bounds__(32 * NW)
         }
         cp_commit();
     };
-    load_kv(0, 0);
-    cp_wait<1>();
+#pragma unroll
+    for (int j = 0; j < KS - 1; ++j) load_kv(j, j);
+    cp_wait<KS - 1>();  // Q landed (the K/V prologue groups may be in flight)
     __syncthreads();
     // Q fragments of this warp's 16 rows (kept in registers)
     uint32_t qf[D / 16][4];
@@ -194,9 +209,9 @@ __global__ void __launch_bounds__(32 * NW)
     float mrow[2] = {-FLT_MAX, -FLT_MAX}, lrow[2] = {0.f, 0.f};
     const int qa = q0 + warp * 16 + (lane >> 2);  // this thread's query rows qa, qa + 8
     for (int j = 0; j < nkv; ++j) {
-        const int stg = j & 1;
-        if (j + 1 < nkv) load_kv(j + 1, stg ^ 1);
-        if (j + 1 < nkv) cp_wait<1>(); else cp_wait<0>();
+        const int stg = j % KS;
+        load_kv(j + KS - 1, (j + KS - 1) % KS);  // refills the stage consumed last iteration
+        cp_wait<KS - 1>();                       // key tile j landed
         __syncthreads();
         const uint32_t kb = smem_addr(sK + stg * BC * D * 2), vb = smem_addr(sV + stg * BC * D * 2);
         // S = Q K^T : 16 x 64 per warp, 8 n-tiles
@@ -516,8 +531,7 @@ __global__ void synth_tokens_kernel(int32_t* out, int64_t n, uint64_t seed, int6
 // 4 warps x 16 query rows: 80 KB at D = 128 (2 CTAs per SM); 8 warps
 // would not raise occupancy: at 186 registers one 256-thread CTA fills the
 // register file
-constexpr int kPrefillWarps = 4;
-int attn_prefill_smem(int D) { return (16 * kPrefillWarps * D * 2) + 4 * (64 * D * 2); }
+int attn_prefill_smem(int D) { return (16 * kPrefillWarps * D * 2) + 2 * kPrefillStages * (64 * D * 2); }
 
 cudaError_t launch_embed(const int32_t* tok, int rows, int pos0, int pos_per_req, int s_tokens,
                          const void* E, const void* P, int pos_s, int h, int64_t vocab, void* x,
@@ -538,7 +552,7 @@ cudaError_t launch_attn_prefill(const void* qkv, int reqs, int s, int h, int D, 
     __nv_bfloat16* k = static_cast<__nv_bfloat16*>(kc);
     __nv_bfloat16* v = static_cast<__nv_bfloat16*>(vc);
     void* args[] = {&q, &s, &h, const_cast<float*>(&scale_log2), &o, &k, &v, &req0, &S_max};
-    const dim3 grid((s + 16 * kPrefillWarps - 1) / (16 * kPrefillWarps), h / D, reqs);
+    const dim3 grid(h / D, reqs, (s + 16 * kPrefillWarps - 1) / (16 * kPrefillWarps));
     const int smem = attn_prefill_smem(D);
     const void* fn;
     if (D == 128) {
