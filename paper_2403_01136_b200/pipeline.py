@@ -8,17 +8,18 @@ from __future__ import annotations
 
 import ctypes as C
 import json
-import os
 from dataclasses import dataclass
 from pathlib import Path
 
 from . import capi
 from .capi import check, lib
 
-# NCCL caches its parameters when it first initialises in the process: set
-# the executor's P2P channel cap (pipeline.cpp build()) before anything --
-# e.g. torch.distributed with the nccl backend -- creates a communicator.
-os.environ.setdefault("NCCL_MAX_P2P_NCHANNELS", "2")
+# The executor caps NCCL P2P channels at 2 per link (pipeline.cpp, only for
+# world > 1 and only if the caller has not set NCCL_MAX_P2P_NCHANNELS). NCCL
+# reads it at its first initialisation in the process, so a host that
+# creates NCCL communicators before the Pipeline (torch.distributed with the
+# nccl backend) sets it itself -- bench.py does; importing this module does
+# not touch the environment.
 
 ROOT = Path(__file__).resolve().parents[1]
 PLANS = ROOT / "tests" / "golden" / "plans"
