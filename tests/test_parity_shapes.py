@@ -2,7 +2,8 @@
 
 Every op of the OPT-13B (bench, BASELINE configs[1]) and OPT-30B
 (north_star target) decoder layer -- qkv [3h1 x h1], out [h1 x h1],
-fc1 [h2 x h1], fc2 [h1 x h2] -- at 3/4/8/16 bits x {asym, sym}, through
+fc1 [h2 x h1], fc2 [h1 x h2] -- at 3/4/8/16 bits x {asym, sym} (and of the
+OPT-66B / BLOOM-176B layers, configs[3..4], at 3 asym / 4, 8, 16 sym), through
 K3 (decode, m = xi = 32, stream-K) and K4 (prefill, m = eta*s = 2048; out /
 fc2 take the stream-K prefill split there), against the CPU oracle:
 
@@ -62,15 +63,22 @@ def _err(got, ref):
     return float(np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-30))
 
 
-@pytest.mark.parametrize("bits,scheme", BITS_SCHEMES, ids=[f"b{b}s{s}" for b, s in BITS_SCHEMES])
+# configs[3] / configs[4] layer shapes (OPT-66B, BLOOM-176B; their 8-stage
+# plans use 3/4/8/16 bits): one bit width per scheme family, every op
+MODELS_BIG = {"opt66b": (9216, 36864), "bloom176b": (14336, 57344)}
+BITS_SCHEMES_BIG = [(3, 0), (4, 1), (8, 1), (16, 1)]
+CASES = ([(m, b, s) for m in MODELS for b, s in BITS_SCHEMES] +
+         [(m, b, s) for m in MODELS_BIG for b, s in BITS_SCHEMES_BIG])
+
+
+@pytest.mark.parametrize("model,bits,scheme", CASES, ids=[f"{m}-b{b}s{s}" for m, b, s in CASES])
 @pytest.mark.parametrize("op", list(OPS))
-@pytest.mark.parametrize("model", list(MODELS))
 def test_benched_shape_k1_k3_k4_vs_oracle(cuda, model, op, bits, scheme):
     import torch
 
     import oracle
     from paper_2403_01136_b200 import qweight
-    h1, h2 = MODELS[model]
+    h1, h2 = {**MODELS, **MODELS_BIG}[model]
     n, k = OPS[op](h1, h2)
     seed = zlib.crc32(f"{model}/{op}/{bits}/{scheme}".encode()) % 2**31
     rng = np.random.default_rng(seed)
