@@ -61,6 +61,9 @@
 #define HP_DEC_CORES 0
 #endif
 // stream-K straggler reduction of the CTA's final segment via bulk copies
+#ifndef HP_SK_FAST_FIN
+#define HP_SK_FAST_FIN 1  // final-segment reduction without the publish (round 2)
+#endif
 #ifndef HP_SK_TMA_RED
 #define HP_SK_TMA_RED 1  // 40-layer OPT-13B plan decode step 3267 -> 3152 us (round 2)
 #endif
@@ -117,6 +120,18 @@ struct qgemm_args {
     unsigned* counters; // [tiles]
     unsigned long long* trace;  // optional per-role clock trace of CTA 0
 };
+
+// per-CTA timestamp slot k (HP_QGEMM_TRACE builds): final-segment epilogue events
+#ifdef HP_QGEMM_TRACE
+#define HP_TRACE_CTA(a, k, v) do { if ((a).trace) (a).trace[6 * 64 * 4 + (5 + (k)) * 1024 + blockIdx.x] = (v); } while (0)
+#else
+#define HP_TRACE_CTA(a, k, v) do { } while (0)
+#endif
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 // Debug trace (HP_QGEMM_TRACE): CTA 0 records %globaltimer at pipeline
 // events: slot = role*kTraceIters*4 + iter*4 + event.
@@ -395,6 +410,7 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NACC);
     unsigned* bcast = tmem_slot + 1;
     uint64_t* redbar = reinterpret_cast<uint64_t*>(tmem_slot + 2);  // final-segment reduction
+    unsigned* s_fastfin = reinterpret_cast<unsigned*>(redbar + 1);   // HP_SK_FAST_FIN flag
 
     // warp index broadcast from lane 0: provably warp-uniform for the
     // compiler, so role code runs on the uniform datapath (no R2UR)
@@ -683,6 +699,16 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
         const uint32_t lane_addr = static_cast<uint32_t>(lq * 32) << 16;
         uint32_t ut = 0, git = 0;
         while (iter.next(a, sg)) {
+            [[maybe_unused]] bool tr_final = false;  // HP_QGEMM_TRACE: this CTA's final segment
+            // fastfin: see HP_SK_FAST_FIN below. Kept in SMEM and re-read at each
+            // use (a register live across the segment pushed the kernel past
+            // its 96-register cap: 140 B of spills in every role)
+            if (warp == C::kEpiWarp0 && lane == 0) *s_fastfin = 0u;
+            auto fastfin_now = [&]() {
+                unsigned v;
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(s_fastfin)));
+                return v != 0u;
+            };
             const int mt = tile_mt(a, sg.tile), nt = tile_nt(a, sg.tile);
             const int acc = ut % NACC;
             constexpr bool kSK = true;  // stream-K: decode tiles, and wave-quantised prefill ops
@@ -750,26 +776,59 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
                 }
             } else {
             trace_ev(a, warp == C::kEpiWarp0 && lane == 0 ? 3 : 99, 48 + ut, 0);
+            // Fast final reduction (HP_SK_FAST_FIN): a CTA's final segment
+            // usually closes a tile whose other segments their CTAs computed
+            // FIRST (seg_iter order). If the tile counter already shows all of
+            // them, this segment skips its partial store to global memory and
+            // the gpu-scope release + ticket (~1.6 us on the kernel tail,
+            // tools/trace_qgemm.py): its accumulator goes to its own slot of
+            // the bulk-copy reduction buffer in SMEM and the shared summation
+            // below adds all segments in order -- bit-identical.
+#if HP_SK_FAST_FIN
+            if (kSK && sg.nseg > 1 && BN <= 32 && sg.nseg * BN * 128 * 4 <= BR * C::kB && a.dp == 0 &&
+                iter.at_end()) {
+                if (warp == C::kEpiWarp0 && lane == 0) {
+                    unsigned c;
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(&a.counters[sg.tile]) : "memory");
+                    *bcast = c;
+                }
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (warp == C::kEpiWarp0 && lane == 0) *s_fastfin = *bcast == static_cast<unsigned>(sg.nseg - 1);
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+            }
+#endif
             mbar_wait(&tfull[acc], (ut / NACC) & 1);
             trace_ev(a, warp == C::kEpiWarp0 && lane == 0 ? 3 : 99, 48 + ut, 1);
+            tr_final = warp == C::kEpiWarp0 && lane == 0 && iter.at_end();
+            if (tr_final) HP_TRACE_CTA(a, 0, gtimer());
             tc_fence_after();
+            constexpr uint32_t kSegB = BN * 128 * 4;  // one segment's fp32 partial tile
+            if (warp == C::kEpiWarp0 && fastfin_now()) {  // the rings are idle: this CTA's MMAs are all done
+                const uint8_t* src = reinterpret_cast<const uint8_t*>(a.partial) +
+                                     static_cast<size_t>(sg.tile) * a.maxseg * kSegB;
+                asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> bulk-copy reads
+                mbar_arrive_expect_tx_elect(redbar, (sg.nseg - 1) * kSegB);
+                for (int j = 0; j < sg.nseg; ++j)
+                    if (j != sg.idx) bulk_g2s_elect(stage_b(0) + j * kSegB, src + j * kSegB, kSegB, redbar);
+            }
             // partials: [tile][seg][BN/4][128 rows] float4 -- row r is the
-            // thread, so every warp access is 512 contiguous bytes
+            // thread, so every warp access is 512 contiguous bytes (global, or
+            // this CTA's own slot of the SMEM reduction buffer when fastfin)
             float4* part = (kSK && sg.nseg > 1)
-                               ? reinterpret_cast<float4*>(a.partial) +
-                                     (static_cast<size_t>(sg.tile) * a.maxseg + sg.idx) * (BN / 4) * 128 + r
+                               ? (fastfin_now() ? reinterpret_cast<float4*>(stage_b(0) + sg.idx * kSegB) + r
+                                          : reinterpret_cast<float4*>(a.partial) +
+                                                (static_cast<size_t>(sg.tile) * a.maxseg + sg.idx) * (BN / 4) * 128 + r)
                                : nullptr;
 #pragma unroll 1
             for (int c0 = 0; c0 < BN; c0 += 16) {
                 uint32_t v[16];
                 tmem_ld16(tmem + lane_addr + acc * BN + c0, v);
                 tmem_ld_wait();
-                if (kSK && part) {
+                if (kSK && part) {  // generic stores: global partials, or the SMEM slot (fastfin)
 #pragma unroll
                     for (int i = 0; i < 16; i += 4)
-                        __stcg(part + ((c0 + i) / 4) * 128,
-                               make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
-                                           __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3])));
+                        part[((c0 + i) / 4) * 128] = make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
+                                                                 __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
                 } else {
                     float f[16];
 #pragma unroll
@@ -782,6 +841,7 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
             if (lane == 0) mbar_arrive(&tempty[acc]);
             }
             trace_ev(a, warp == C::kEpiWarp0 && lane == 0 ? 3 : 99, 48 + ut, 2);
+            if (tr_final) HP_TRACE_CTA(a, 1, gtimer());
 
             if constexpr (kSK) if (sg.nseg > 1) {
                 const int tr5 = warp == C::kEpiWarp0 && lane == 0 ? 5 : 99;
@@ -791,28 +851,35 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
                 // CUTLASS split-K semaphore pattern; one gpu-scope
                 // synchronisation instead of a fence.sc in every thread
                 trace_ev(a, tr5, ut, 0);
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-                if (warp == C::kEpiWarp0 && lane == 0) {
-                    unsigned old;
-                    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
-                                 : "=r"(old) : "l"(&a.counters[sg.tile]) : "memory");
-                    *bcast = old;
+                if (!fastfin_now()) {
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    if (warp == C::kEpiWarp0 && lane == 0) {
+                        unsigned old;
+                        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                                     : "=r"(old) : "l"(&a.counters[sg.tile]) : "memory");
+                        *bcast = old;
+                    }
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
                 }
-                asm volatile("bar.sync 1, 128;" ::: "memory");
                 trace_ev(a, tr5, ut, 1);
+                if (tr_final) {
+                    HP_TRACE_CTA(a, 2, gtimer());
+                    HP_TRACE_CTA(a, 3, static_cast<unsigned long long>(sg.nseg * 100 + (*bcast == static_cast<unsigned>(sg.nseg - 1) ? 10 : 0)));
+                }
                 bool tma_red = false;
 #if HP_SK_TMA_RED
                 // The straggler's reduction is usually the CTA's FINAL segment:
                 // every MMA of the CTA has completed, so the activation ring is
                 // idle. Pull all nseg partials (16 KB each at BN = 32) into it
                 // with bulk copies -- one L2 round trip -- and sum from SMEM.
-                tma_red = *bcast == static_cast<unsigned>(sg.nseg - 1) && BN <= 32 &&
-                          sg.nseg * BN * 128 * 4 <= BR * C::kB && a.dp == 0 && iter.at_end();
+                tma_red = fastfin_now() || (*bcast == static_cast<unsigned>(sg.nseg - 1) && BN <= 32 &&
+                                      sg.nseg * BN * 128 * 4 <= BR * C::kB && a.dp == 0 && iter.at_end());
                 if (tma_red) {
                     constexpr uint32_t kSeg = BN * 128 * 4;
                     const uint8_t* src = reinterpret_cast<const uint8_t*>(a.partial) +
                                          static_cast<size_t>(sg.tile) * a.maxseg * kSeg;
-                    if (warp == C::kEpiWarp0) {
+                    if (warp == C::kEpiWarp0 && !fastfin_now()) {
+                        asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> bulk-copy reads
                         mbar_arrive_expect_tx_elect(redbar, sg.nseg * kSeg);
                         for (int j = 0; j < sg.nseg; ++j)
                             bulk_g2s_elect(stage_b(0) + j * kSeg, src + j * kSeg, kSeg, redbar);
@@ -1076,8 +1143,8 @@ unsigned long long* trace_buffer() {
         if (getenv("HP_QGEMM_TRACE")) {
             int cta = getenv("HP_QGEMM_TRACE_CTA") ? atoi(getenv("HP_QGEMM_TRACE_CTA")) : 0;
             cudaMemcpyToSymbol(g_trace_cta, &cta, sizeof(int));
-            cudaMalloc(&g_trace, sizeof(unsigned long long) * (6 * kTraceIters * 4 + 5 * 1024));
-            cudaMemset(g_trace, 0, sizeof(unsigned long long) * (6 * kTraceIters * 4 + 5 * 1024));
+            cudaMalloc(&g_trace, sizeof(unsigned long long) * (6 * kTraceIters * 4 + 9 * 1024));
+            cudaMemset(g_trace, 0, sizeof(unsigned long long) * (6 * kTraceIters * 4 + 9 * 1024));
         }
     }
     return g_trace;

@@ -23,7 +23,7 @@ def main():
     for _ in range(3):
         qweight.qlinear(qw, x, phase=1)
     torch.cuda.synchronize()
-    buf = np.zeros(6 * 64 * 4 + 5 * 1024, dtype=np.uint64)
+    buf = np.zeros(6 * 64 * 4 + 9 * 1024, dtype=np.uint64)
     lib.hp_debug_trace(buf.ctypes.data, buf.size)
     cyc = buf[6 * 64 * 4 + 2048:6 * 64 * 4 + 2048 + 148].astype(np.int64)
     cta = buf[6 * 64 * 4:6 * 64 * 4 + 2048].reshape(1024, 2).astype(np.int64)
@@ -48,6 +48,24 @@ def main():
               f"{[int(smid[i]) for i in np.argsort(me)[-5:]]}")
         if "--all" in sys.argv:
             print("  last MMA by CTA:", " ".join(f"{v:.1f}" for v in me))
+    B2 = 6 * 64 * 4 + 5 * 1024
+    nc = len(cta)
+    fin = [buf[B2 + k * 1024:B2 + k * 1024 + nc].astype(np.int64) for k in range(4)]
+    if fin[0].max() > 0 and mend.min() > 0:
+        tf = np.where(fin[0] > 0, (fin[0] - t0c) / 1000, np.nan)
+        st_ = np.where(fin[1] > 0, (fin[1] - t0c) / 1000, np.nan)
+        tk = np.where(fin[2] > 0, (fin[2] - t0c) / 1000, np.nan)
+        kind = fin[3]
+        print(f"  final segment: tfull - lastMMA med {np.nanmedian(tf - me):.2f}; store {np.nanmedian(st_ - tf):.2f}; "
+              f"ticket {np.nanmedian(tk - st_):.2f}; exit - (ticket or store) med "
+              f"{np.nanmedian(ext - np.where(np.isnan(tk), st_, tk)):.2f} us")
+        split = kind > 0
+        last = (kind % 100) >= 10
+        print(f"  final segments split: {int(split.sum())}/{nc}, of which reduced here: {int((split & last).sum())}")
+        slow = np.argsort(ext)[-6:]
+        for i in slow:
+            print(f"    slow CTA {i} sm {int(smid[i])}: lastMMA {me[i]:.2f} tfull {tf[i]:.2f} stored {st_[i]:.2f} "
+                  f"ticket {tk[i]:.2f} exit {ext[i]:.2f} kind {int(kind[i])}")
     span_ns = (cta[:148, 1] - cta[:148, 0]).astype(np.float64)
     print(f"  CTA cycles/ns (implied GHz): median {np.median(cyc / span_ns):.3f}, cycles median {np.median(cyc):.0f}")
     g = torch.cuda.CUDAGraph()
