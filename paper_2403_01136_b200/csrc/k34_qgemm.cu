@@ -163,14 +163,18 @@ struct seg_t {
     int tile, g0, g1, idx, nseg;
 };
 
+// 32-bit stream-K arithmetic: plan_qgemm keeps total * grid < 2^32 (an int64
+// division is ~70 instructions; every role evaluates these per segment, and
+// the epilogue's and MMA warp's segment switches sit on the kernel tail)
 __device__ __forceinline__ int64_t sk_lo(int64_t c, int64_t total, int64_t P) {
-    return (c * total) / P;
+    return static_cast<uint32_t>(c) * static_cast<uint32_t>(total) / static_cast<uint32_t>(P);
 }
 // CTA owning group-step w
 __device__ __forceinline__ int sk_owner(int64_t w, int64_t total, int64_t P) {
-    int64_t c = (w * P) / total;
-    while (c + 1 < P && sk_lo(c + 1, total, P) <= w) ++c;
-    while (c > 0 && sk_lo(c, total, P) > w) --c;
+    const uint32_t t = static_cast<uint32_t>(total), p = static_cast<uint32_t>(P);
+    uint32_t c = static_cast<uint32_t>(w) * p / t;
+    while (c + 1 < p && (c + 1) * t / p <= static_cast<uint32_t>(w)) ++c;
+    while (c > 0 && c * t / p > static_cast<uint32_t>(w)) --c;
     return static_cast<int>(c);
 }
 
@@ -1117,6 +1121,11 @@ qgemm_plan plan_qgemm(int64_t n_out, int64_t k_in, int64_t m, int phase) {
             p.dp = dpw * sms;
             p.total = (tiles - p.dp) * G;
         }
+    }
+    if (p.stream_k && p.total * sms >= (int64_t(1) << 32)) {  // 32-bit seg_iter arithmetic
+        p.stream_k = 0;
+        p.dp = 0;
+        p.total = tiles * G;
     }
     if (p.stream_k) {
         p.grid = static_cast<int>(p.total < sms ? p.total : sms);
