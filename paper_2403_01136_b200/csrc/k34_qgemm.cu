@@ -178,6 +178,115 @@ __device__ __forceinline__ int sk_owner(int64_t w, int64_t total, int64_t P) {
     return static_cast<int>(c);
 }
 
+#ifndef HP_SK_SHORT_FIRST
+#define HP_SK_SHORT_FIRST 1
+#endif
+#if HP_SK_SHORT_FIRST
+// Stream-K visit order: the CTA's partial segments (the tail of the tile its
+// range starts in, the head of the tile it ends in) SHORTEST FIRST, then its
+// full tiles. A split tile is then reduced by the CTA that computes its long
+// part, at the END of that work, with the fast final reduction (its short
+// part was computed first by the neighbour); and no CTA reduces a tile while
+// its own final, short segment is still running -- the measured cause of
+// the slowest CTAs' 6 us tails under the previous order (last range segment
+// first, tools/trace_qgemm.py). Reduction order (by segment index) is
+// unchanged, so results are bit-identical.
+struct seg_iter {
+    // unit mode
+    int u;
+    // stream-K mode: up to two partial segments [ps, pe) in visit order, then
+    // the full tiles [w, fe) (group-step indices; < 2^31, see sk_lo)
+    int ps0, pe0, ps1, pe1, w, fe;
+    int np, k;
+    bool last_ret;  // the segment last returned by next() was the final one
+    __device__ __forceinline__ void init(const qgemm_args& a) {
+        u = blockIdx.x;
+        np = k = 0;
+        last_ret = false;
+        const int G = a.G;
+        const int wlo = static_cast<int>(sk_lo(blockIdx.x, a.total, gridDim.x));
+        const int w1 = static_cast<int>(sk_lo(blockIdx.x + 1, a.total, gridDim.x));
+        w = fe = 0;
+        ps0 = pe0 = ps1 = pe1 = 0;
+        if (w1 <= wlo) return;
+        const int fend = min(w1, (wlo / G + 1) * G);    // end of the first range piece
+        const int lbeg = max(wlo, ((w1 - 1) / G) * G);  // start of the last range piece
+        auto full = [G](int s0, int e0) { return s0 % G == 0 && e0 - s0 == G; };
+        if (fend >= w1) {  // the range lies in one tile
+            if (full(wlo, w1)) {
+                w = wlo;
+                fe = w1;
+            } else {
+                ps0 = wlo;
+                pe0 = w1;
+                np = 1;
+            }
+            return;
+        }
+        int fs = fend, fe2 = lbeg;
+        if (full(wlo, fend)) {
+            fs = wlo;
+        } else {
+            ps0 = wlo;
+            pe0 = fend;
+            np = 1;
+        }
+        if (full(lbeg, w1)) {
+            fe2 = w1;
+        } else if (np == 0) {
+            ps0 = lbeg;
+            pe0 = w1;
+            np = 1;
+        } else {
+            ps1 = lbeg;
+            pe1 = w1;
+            np = 2;
+            if (pe1 - ps1 < pe0 - ps0) {  // shorter first
+                const int t0 = ps0, t1 = pe0;
+                ps0 = ps1;
+                pe0 = pe1;
+                ps1 = t0;
+                pe1 = t1;
+            }
+        }
+        w = fs;
+        fe = fe2;
+    }
+    __device__ __forceinline__ bool at_end() const { return last_ret; }
+    __device__ __forceinline__ bool next(const qgemm_args& a, seg_t& s) {
+        if (!a.stream_k || u < a.dp) {
+            const int lim = a.stream_k ? a.dp : a.MT * a.NT;
+            if (u < lim) {
+                s = {u, 0, a.G, 0, 1};
+                u += gridDim.x;
+                return true;
+            }
+            if (!a.stream_k) return false;
+            u = lim;  // data-parallel waves done -> the stream-K region
+        }
+        int s0, e0;
+        if (k < np) {
+            s0 = k == 0 ? ps0 : ps1;
+            e0 = k == 0 ? pe0 : pe1;
+            ++k;
+        } else if (w < fe) {
+            s0 = w;
+            e0 = w + a.G;
+            w = e0;
+        } else {
+            return false;
+        }
+        last_ret = k >= np && w >= fe;
+        const int tile = s0 / a.G;  // within the stream-K region
+        const int g0 = s0 - tile * a.G;
+        const int64_t tend = static_cast<int64_t>(tile + 1) * a.G;
+        const int first = sk_owner(static_cast<int64_t>(tile) * a.G, a.total, gridDim.x);
+        const int last = sk_owner(tend - 1, a.total, gridDim.x);
+        s = {a.dp + tile, g0, g0 + (e0 - s0), static_cast<int>(blockIdx.x) - first, last - first + 1};
+        return true;
+    }
+};
+#else
 // Stream-K segments are visited with the CTA's LAST segment first: the head
 // of the tile that the next CTA finishes early, so both halves of every
 // split tile complete (and get reduced) early instead of at the kernel tail.
@@ -231,6 +340,8 @@ struct seg_iter {
         return true;
     }
 };
+
+#endif
 
 // A pipeline stage covers SPS 32-k "slices" (SPS = 8: two 128-k groups,
 // decode; SPS = 2: half a group, prefill — keeps the [BN x K] activation
