@@ -1087,7 +1087,12 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
             trace_ev(a, warp == C::kEpiWarp0 && lane == 0 ? 3 : 99, 48 + ut, 3);
             ++ut;
         }
+        if (warp == C::kEpiWarp0 && lane == 0) HP_TRACE_CTA(a, 4, gtimer());
     }
+#ifdef HP_QGEMM_TRACE
+    if (lane == 0 && (warp == 0 || warp == 3 || warp == 4))  // role loop exits: producer, act producer, dequant w4
+        HP_TRACE_CTA(a, warp == 0 ? 6 : (warp == 3 ? 5 : 7), gtimer());
+#endif
 
     __syncthreads();
 #ifdef HP_QGEMM_TRACE
@@ -1263,8 +1268,8 @@ unsigned long long* trace_buffer() {
         if (getenv("HP_QGEMM_TRACE")) {
             int cta = getenv("HP_QGEMM_TRACE_CTA") ? atoi(getenv("HP_QGEMM_TRACE_CTA")) : 0;
             cudaMemcpyToSymbol(g_trace_cta, &cta, sizeof(int));
-            cudaMalloc(&g_trace, sizeof(unsigned long long) * (6 * kTraceIters * 4 + 9 * 1024));
-            cudaMemset(g_trace, 0, sizeof(unsigned long long) * (6 * kTraceIters * 4 + 9 * 1024));
+            cudaMalloc(&g_trace, sizeof(unsigned long long) * (6 * kTraceIters * 4 + 13 * 1024));
+            cudaMemset(g_trace, 0, sizeof(unsigned long long) * (6 * kTraceIters * 4 + 13 * 1024));
         }
     }
     return g_trace;

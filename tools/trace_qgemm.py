@@ -23,7 +23,7 @@ def main():
     for _ in range(3):
         qweight.qlinear(qw, x, phase=1)
     torch.cuda.synchronize()
-    buf = np.zeros(6 * 64 * 4 + 9 * 1024, dtype=np.uint64)
+    buf = np.zeros(6 * 64 * 4 + 13 * 1024, dtype=np.uint64)
     lib.hp_debug_trace(buf.ctypes.data, buf.size)
     cyc = buf[6 * 64 * 4 + 2048:6 * 64 * 4 + 2048 + 148].astype(np.int64)
     cta = buf[6 * 64 * 4:6 * 64 * 4 + 2048].reshape(1024, 2).astype(np.int64)
@@ -50,7 +50,7 @@ def main():
             print("  last MMA by CTA:", " ".join(f"{v:.1f}" for v in me))
     B2 = 6 * 64 * 4 + 5 * 1024
     nc = len(cta)
-    fin = [buf[B2 + k * 1024:B2 + k * 1024 + nc].astype(np.int64) for k in range(4)]
+    fin = [buf[B2 + k * 1024:B2 + k * 1024 + nc].astype(np.int64) for k in range(8)]
     if fin[0].max() > 0 and mend.min() > 0:
         tf = np.where(fin[0] > 0, (fin[0] - t0c) / 1000, np.nan)
         st_ = np.where(fin[1] > 0, (fin[1] - t0c) / 1000, np.nan)
@@ -64,8 +64,10 @@ def main():
         print(f"  final segments split: {int(split.sum())}/{nc}, of which reduced here: {int((split & last).sum())}")
         slow = np.argsort(ext)[-6:]
         for i in slow:
+            rel = [(fin[k][i] - t0c) / 1000 if fin[k][i] > 0 else float("nan") for k in (4, 5, 6, 7)]
             print(f"    slow CTA {i} sm {int(smid[i])}: lastMMA {me[i]:.2f} tfull {tf[i]:.2f} stored {st_[i]:.2f} "
-                  f"ticket {tk[i]:.2f} exit {ext[i]:.2f} kind {int(kind[i])}")
+                  f"ticket {tk[i]:.2f} exit {ext[i]:.2f} kind {int(kind[i])} | loop exits: epi {rel[0]:.2f} "
+                  f"act {rel[1]:.2f} prod {rel[2]:.2f} dq {rel[3]:.2f}")
     span_ns = (cta[:148, 1] - cta[:148, 0]).astype(np.float64)
     print(f"  CTA cycles/ns (implied GHz): median {np.median(cyc / span_ns):.3f}, cycles median {np.median(cyc):.0f}")
     g = torch.cuda.CUDAGraph()
