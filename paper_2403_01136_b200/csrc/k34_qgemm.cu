@@ -999,6 +999,16 @@ __global__ void __launch_bounds__(qgemm_cfg<BITS, BN, SPS>::kThreads,
                         for (int j = 0; j < sg.nseg; ++j)
                             bulk_g2s_elect(stage_b(0) + j * kSeg, src + j * kSeg, kSeg, redbar);
                     }
+                    if (a.res) {  // the residual rows this thread adds in stage_store16: into L1 while the copies land
+                        const int tid = threadIdx.x & 127;
+                        const int n = nt * 128 + (tid & 7) * 16;
+#pragma unroll
+                        for (int c0 = 0; c0 < BN; c0 += 16) {
+                            const int tok = mt * BN + c0 + (tid >> 3);
+                            if (tok < a.m && n < a.n_out)
+                                asm volatile("prefetch.global.L1 [%0];" ::"l"(a.res + static_cast<int64_t>(tok) * a.ldr + n));
+                        }
+                    }
                     mbar_wait(redbar, 0);  // once per CTA: its final segment
                     const float4* sp = reinterpret_cast<const float4*>(stage_b(0)) + r;
 #pragma unroll 1
