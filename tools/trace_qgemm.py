@@ -21,7 +21,7 @@ def main():
     qw = qweight.quantize(w, bits)
     x = torch.randn(m, k, device=dev).to(torch.bfloat16)
     for _ in range(3):
-        qweight.qlinear(qw, x, phase=1)
+        qweight.qlinear(qw, x, phase=(0 if m > 64 else 1))
     torch.cuda.synchronize()
     buf = np.zeros(6 * 64 * 4 + 13 * 1024, dtype=np.uint64)
     lib.hp_debug_trace(buf.ctypes.data, buf.size)
@@ -73,11 +73,11 @@ def main():
     g = torch.cuda.CUDAGraph()
     st = torch.cuda.Stream()
     with torch.cuda.stream(st):
-        qweight.qlinear(qw, x, phase=1)
+        qweight.qlinear(qw, x, phase=(0 if m > 64 else 1))
         torch.cuda.synchronize()
         with torch.cuda.graph(g, stream=st):
             for _ in range(10):
-                qweight.qlinear(qw, x, phase=1)
+                qweight.qlinear(qw, x, phase=(0 if m > 64 else 1))
     g.replay(); torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(); g.replay(); e1.record(); torch.cuda.synchronize()
