@@ -27,12 +27,15 @@ H1, H2, HEADS, VOCAB, POS = 768, 3072, 12, 50272, 2050
 SHAPES = [(3 * H1, H1), (H1, H1), (H2, H1), (H1, H2)]
 
 
-def _plan(n=4, eta=None):
+def _plan(n=4, eta=None, xi=None):
     from paper_2403_01136_b200.pipeline import load_plan
     plan_json, model_json = load_plan("opt125m_b8_1gpu")
     plan = json.loads(plan_json)
     plan["workload"]["n"] = n  # xi == B: the objective does not depend on n
-    if eta is not None:  # re-batch the prefill; recompose Eq. (4) (types.cpp:17-24)
+    if xi is not None:  # several decode groups (the last one ragged when B % xi != 0)
+        plan["xi"] = xi
+    if eta is not None or xi is not None:  # re-batch; recompose Eq. (4) (types.cpp:17-24)
+        eta = plan["eta"] if eta is None else eta
         plan["eta"] = eta
         o, B = plan["objective"], plan["workload"]["global_bz"]
         bc = lambda u: -(-(B - u) // u)
@@ -127,16 +130,19 @@ def _final_hidden(pipe, B):
     return h.reshape(B, H1)
 
 
-@pytest.mark.parametrize("graphs,eta", [(True, None), (False, None), (True, 3)])
-def test_opt125m_round_matches_reference_decoder(cuda, graphs, eta):
+@pytest.mark.parametrize("graphs,eta,xi", [(True, None, None), (False, None, None), (True, 3, None),
+                                           (True, None, 3)])
+def test_opt125m_round_matches_reference_decoder(cuda, graphs, eta, xi):
     """eta = 3 with B = 8: a ragged last prefill micro-batch (3, 3, 2), the
-    case whose stream-K workspace was once undersized."""
+    case whose stream-K workspace was once undersized. xi = 3:
+    three decode groups (3, 3, 2) interleaved by the schedule, the last one
+    ragged -- different K3 tile widths and KV-cache request offsets per group."""
     import torch
 
     from oracle import synth
     from paper_2403_01136_b200.pipeline import Pipeline
     n = 4
-    plan, model_json = _plan(n, eta)
+    plan, model_json = _plan(n, eta, xi)
     B, s = 8, 512
     pipe = Pipeline(json.dumps(plan), model_json, use_graphs=graphs, instrument=True)
     gen = _run(pipe, B, n)
