@@ -314,6 +314,16 @@ def main():
             return ({"captured_launches": e["launches"], "alg_bytes_per_launch": e["alg_bytes_per_launch"],
                      "source": e["source"]} if e else None)
         pre_share = pre_busy / (pre_busy + dec_busy) if pre_busy + dec_busy > 0 else 0
+        launches = ROOT / "profiles" / "launches_r02.json"
+
+        def launch_share(cls):  # the kernel class's share of the round in the committed ncu launch list
+            if not launches.exists():
+                return None
+            ex = json.loads(launches.read_text()).get("round_extrapolation", {})
+            if ex.get("plan") != name:
+                return None
+            e = ex.get("classes", {}).get(cls)
+            return {"share": e["share"], "source": "profiles/launches_r02.json"} if e else None
         roof_pre = {"kernel": "K4 prefill dequant-GEMM (hp::qgemm_kernel, BN=256)",
                     # the burst peak: K4 inside the round already exceeds the
                     # "sustained" cuBLAS figure, which is therefore no ceiling
@@ -325,7 +335,10 @@ def main():
                     "per_launch": {"launches": d_pre["launches"],
                                    "avg_flops": d_pre["flops"] / max(d_pre["launches"], 1),
                                    "avg_s": d_pre["seconds"] / max(d_pre["launches"], 1)},
-                    "share_of_step": pre_share}
+                    # the PHASE share (prefill units incl. their LN / attention);
+                    # the kernel's own share comes from the ncu launch list
+                    "phase_share_of_step": pre_share,
+                    "launch_list_share": launch_share("K4 prefill qgemm (BN>=128)")}
         roof_dec = {"kernel": "K3 decode dequant-GEMV (hp::qgemm_kernel, BN=32, split-K)",
                     "bound": "hbm", "achieved": k3, "peak": hbm, "unit": "GB/s",
                     "frac": k3 / hbm if k3 else None, "frac_of_nominal_8TBs": k3 / 8000 if k3 else None,
@@ -334,7 +347,8 @@ def main():
                     "per_launch": {"launches": d_dec["launches"],
                                    "avg_bytes": d_dec["bytes"] / max(d_dec["launches"], 1),
                                    "avg_s": d_dec["seconds"] / max(d_dec["launches"], 1)},
-                    "share_of_step": 1 - pre_share}
+                    "phase_share_of_step": 1 - pre_share,
+                    "launch_list_share": launch_share("K3 decode qgemm (BN<=64)")}
         dominant, other = (roof_pre, roof_dec) if pre_share >= 0.5 else (roof_dec, roof_pre)
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
