@@ -314,12 +314,12 @@ def main():
             return ({"captured_launches": e["launches"], "alg_bytes_per_launch": e["alg_bytes_per_launch"],
                      "source": e["source"]} if e else None)
         pre_share = pre_busy / (pre_busy + dec_busy) if pre_busy + dec_busy > 0 else 0
-        launches = ROOT / "profiles" / "launches_r02.json"
+        launch_list = ROOT / "profiles" / "launches_r02.json"
 
         def launch_share(cls):  # the kernel class's share of the round in the committed ncu launch list
-            if not launches.exists():
+            if not launch_list.exists():
                 return None
-            ex = json.loads(launches.read_text()).get("round_extrapolation", {})
+            ex = json.loads(launch_list.read_text()).get("round_extrapolation", {})
             if ex.get("plan") != name:
                 return None
             e = ex.get("classes", {}).get(cls)
