@@ -186,6 +186,46 @@ __device__ __forceinline__ uint32_t finish_pair(uint32_t v, uint32_t negoff2,
     return d;
 }
 
+// bf16x2 product a * b, one rounding (-0 addend keeps the sign of zero)
+__device__ __forceinline__ uint32_t bf16x2_mul(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(0x80008000u));
+    return d;
+}
+
+// 8-bit pair: fp32 magic words (2^23 + code) -> (m + negoff) exactly, then
+// * s (symmetric) or fma(., s, z) (asymmetric) as f32x2, rounded to bf16x2
+template <bool SYM>
+__device__ __forceinline__ uint32_t magic8_pair(uint32_t m0, uint32_t m1, float negoff, float s,
+                                                float z) {
+    uint32_t d;
+    if constexpr (SYM) {
+        asm("{\n\t.reg .b64 a, o, sc, r;\n\t.reg .b32 rl, rh;\n\t"
+            "mov.b64 a, {%1, %2};\n\t"
+            "mov.b64 o, {%3, %3};\n\t"
+            "mov.b64 sc, {%4, %4};\n\t"
+            "add.rn.f32x2 a, a, o;\n\t"
+            "mul.rn.f32x2 r, a, sc;\n\t"
+            "mov.b64 {rl, rh}, r;\n\t"
+            "cvt.rn.bf16x2.f32 %0, rh, rl;\n\t}"
+            : "=r"(d)
+            : "r"(m0), "r"(m1), "f"(negoff), "f"(s));
+    } else {
+        asm("{\n\t.reg .b64 a, o, sc, zz, r;\n\t.reg .b32 rl, rh;\n\t"
+            "mov.b64 a, {%1, %2};\n\t"
+            "mov.b64 o, {%3, %3};\n\t"
+            "mov.b64 sc, {%4, %4};\n\t"
+            "mov.b64 zz, {%5, %5};\n\t"
+            "add.rn.f32x2 a, a, o;\n\t"
+            "fma.rn.f32x2 r, a, sc, zz;\n\t"
+            "mov.b64 {rl, rh}, r;\n\t"
+            "cvt.rn.bf16x2.f32 %0, rh, rl;\n\t}"
+            : "=r"(d)
+            : "r"(m0), "r"(m1), "f"(negoff), "f"(s), "f"(z));
+    }
+    return d;
+}
+
 // Raw code words of one 32-element slice (loaded ahead of the conversion so
 // the shared-memory latency of all slices overlaps).
 template <int BITS>
@@ -230,6 +270,33 @@ __device__ __forceinline__ void convert_slice(const slice_words<BITS>& in, float
             for (int p = 0; p < 4; ++p)
                 out[4 * j + p] = finish_pair<SYM, RAW>(
                     lop3_and_or(in.w[j] >> (4 * p), 0x000F000Fu, kMagic128), negoff2, s2, z2);
+    } else if constexpr (BITS == 3 && SYM && !RAW) {
+        // Fewer shifts: a 3-bit code anywhere in bits 0..6 of a half-word
+        // ORs into the bf16 magic exactly (128 + 2^j q <= 240 stays in the
+        // [128, 256) binade). Codes at bits 3..5 give v = 128 + 8q, and
+        // (v - (128 + 8 hi)) * (bf16(s) / 8) = 8 (q - hi) * bf16(s) / 8 is
+        // the same real product as (q - hi) * bf16(s), rounded once: the
+        // result is bit-identical to the one-shift-per-code form, with 8
+        // instead of 15 shifts per 16 pairs (w, w >> 6, w >> 12 expose
+        // codes 0/1, 2/3 and 4 of each half).
+        constexpr uint32_t negoff2 = 0xC303C303u;   // -(128 + 3)
+        constexpr uint32_t negoff8 = 0xC318C318u;   // -(128 + 8 * 3)
+        const uint32_t s8 = bf16x2_mul(s2, 0x3E003E00u);  // bf16(s) / 8, exact
+#pragma unroll
+        for (int w = 0; w < 3; ++w) {
+            const uint32_t a = in.w[w], b = a >> 6, c = a >> 12;
+            out[5 * w + 0] = finish_pair<true>(lop3_and_or(a, 0x00070007u, kMagic128), negoff2, s2, z2);
+            out[5 * w + 1] = finish_pair<true>(lop3_and_or(a, 0x00380038u, kMagic128), negoff8, s8, z2);
+            out[5 * w + 2] = finish_pair<true>(lop3_and_or(b, 0x00070007u, kMagic128), negoff2, s2, z2);
+            out[5 * w + 3] = finish_pair<true>(lop3_and_or(b, 0x00380038u, kMagic128), negoff8, s8, z2);
+            out[5 * w + 4] = finish_pair<true>(lop3_and_or(c, 0x00070007u, kMagic128), negoff2, s2, z2);
+        }
+        // bit 15 of each half of the three words = code 15's bits 0, 1, 2,
+        // gathered at bits 3, 4, 5 (w0 >> 12 is already there)
+        uint32_t t = lop3_and_or(in.w[0] >> 12, 0x00080008u, kMagic128);
+        t = lop3_and_or(in.w[1] >> 11, 0x00100010u, t);
+        t = lop3_and_or(in.w[2] >> 10, 0x00200020u, t);
+        out[15] = finish_pair<true>(t, negoff8, s8, z2);
     } else if constexpr (BITS == 3) {
         constexpr uint32_t negoff2 = SYM ? 0xC303C303u : 0xC300C300u;
 #pragma unroll
@@ -247,11 +314,16 @@ __device__ __forceinline__ void convert_slice(const slice_words<BITS>& in, float
         for (int j = 0; j < 8; ++j)
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
-                const float f0 = __uint_as_float(prmt(in.w[j], 0x4B000000u, 0x7540u + 2 * p)) - off;
-                const float f1 = __uint_as_float(prmt(in.w[j], 0x4B000000u, 0x7541u + 2 * p)) - off;
-                const float d0 = RAW ? f0 : (SYM ? f0 * s : __fmaf_rn(f0, s, z));
-                const float d1 = RAW ? f1 : (SYM ? f1 * s : __fmaf_rn(f1, s, z));
-                out[2 * j + p] = pack_bf16x2(d0, d1);
+                const uint32_t m0 = prmt(in.w[j], 0x4B000000u, 0x7540u + 2 * p);
+                const uint32_t m1 = prmt(in.w[j], 0x4B000000u, 0x7541u + 2 * p);
+                if constexpr (RAW) {
+                    out[2 * j + p] = pack_bf16x2(__uint_as_float(m0) - off, __uint_as_float(m1) - off);
+                } else {
+                    // the per-element fp32 arithmetic (exact magic - off, then
+                    // * s or fma(., s, z), one bf16 rounding) on f32x2 pairs:
+                    // bit-identical, 5 instead of 7 instructions per pair
+                    out[2 * j + p] = magic8_pair<SYM>(m0, m1, -off, s, z);
+                }
             }
     } else {
 #pragma unroll
