@@ -35,6 +35,13 @@
 #include "layout.cuh"
 #include "sm100.cuh"
 
+// HP_PRE_BN192: prefill token tiles of 192 with a double-buffered
+// accumulator (2 x 192 of the 512 TMEM columns, 4 A stages in the rest), so
+// a tile's epilogue overlaps the next tile's MMAs; 2048-token ops then split
+// into 11 token tiles (out / fc2: 440 tiles = 2.97 waves, no stream-K).
+#ifndef HP_PRE_BN192
+#define HP_PRE_BN192 0
+#endif
 #ifndef HP_DEC_SPS
 #define HP_DEC_SPS 8
 #endif
@@ -380,7 +387,7 @@ struct qgemm_cfg {
     // they consume must always belong to the same warpgroup (depth % DWG ==
     // 0); otherwise an mbarrier parity wait could alias another phase.
     static constexpr int CR = kRR ? (CR_ / DWG) * DWG : CR_;
-    static constexpr int NACC = BN <= 128 ? 2 : 1;
+    static constexpr int NACC = (BN <= 128 || BN == 192) ? 2 : 1;
     static constexpr bool kGSok = kRR && HP_DEC_GS;               // sym kernels only (see kernel)
     static constexpr int GCOLS = kGSok ? 2 * NG * BN : 0;          // 2 stage slots x NG group sums
     static constexpr int A0_ = NACC * BN < 64 ? (GCOLS > 64 ? GCOLS : 64)
@@ -1213,7 +1220,7 @@ qgemm_plan plan_qgemm(int64_t n_out, int64_t k_in, int64_t m, int phase) {
     if (phase == 1 && m <= 32) {
         p.bn = m <= 16 ? 16 : 32;
     } else {
-        p.bn = m <= 128 ? 128 : 256;
+        p.bn = m <= 128 ? 128 : (HP_PRE_BN192 ? 192 : 256);
     }
     p.mt = static_cast<int>(ceil_div64(m, p.bn));
     const int64_t tiles = static_cast<int64_t>(p.mt) * NT;
@@ -1323,6 +1330,9 @@ cudaError_t launch_qgemm(const CUtensorMap& map, const qgemm_plan& p, int bits,
         case 32: return dispatch_bits<32>(bits, sym, map, a, p.grid, st);
         case 128: return dispatch_bits<128>(bits, sym, map, a, p.grid, st);
         case 256: return dispatch_bits<256>(bits, sym, map, a, p.grid, st);
+#if HP_PRE_BN192
+        case 192: return dispatch_bits<192>(bits, sym, map, a, p.grid, st);
+#endif
     }
     return cudaErrorInvalidValue;
 }
