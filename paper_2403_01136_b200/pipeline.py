@@ -7,6 +7,7 @@ rendezvous — all activation traffic is NCCL P2P issued by the C++ runtime).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import json
 from dataclasses import dataclass
 from pathlib import Path
@@ -92,8 +93,10 @@ class Pipeline:
     def __init__(self, plan_json: str, model_json: str, rank: int = 0, world: int = 1,
                  ids: bytes | None = None, scheme: int = capi.HP_SYMMETRIC,
                  use_graphs: bool = True, instrument: bool = False, sm_budget: int = 0,
-                 seed: int = 2403, weight_std: float = 0.02, timeout_s: float = 0.0,
+                 seed: int = 2403, weight_std: float = 0.02, timeout_s: float | None = None,
                  weights: WeightSet | None = None):
+        if timeout_s is None:  # watchdog: a round stuck this long raises instead of hanging
+            timeout_s = float(os.environ.get("HP_PIPELINE_TIMEOUT_S", "0"))
         opt = capi.hp_pipeline_options(scheme, int(use_graphs), int(instrument), sm_budget,
                                        seed, weight_std, timeout_s)
         h = C.c_void_p()
