@@ -996,15 +996,31 @@ struct pipeline::impl {
         run_timing t;
         cuda_ok(cudaEventRecord(ev_t0, cs), "ev");
         load_prompt(host_tokens);
+        // HP_EAGER_PDL=0: launch the eager (uncaptured) rounds without
+        // programmatic dependent launch (diagnostic for the eager-round stall,
+        // DESIGN §8); captured rounds keep it
+        struct pdl_off {
+            bool on;
+            explicit pdl_off(bool e) : on(e) { if (on) hp_set_pdl(0); }
+            ~pdl_off() { if (on) hp_set_pdl(1); }
+        };
+        static const bool eager_no_pdl = [] {
+            const char* e = std::getenv("HP_EAGER_PDL");
+            return e && *e == '0';
+        }();
         if (opt.use_graphs) {
             if (!graph_ready) {
-                enqueue_round();  // eager warm-up (sets kernel attributes)
+                {
+                    pdl_off g(eager_no_pdl);
+                    enqueue_round();  // eager warm-up (sets kernel attributes)
+                }
                 wait_round("warm-up round");
                 load_prompt(host_tokens);
                 capture();
             }
             cuda_ok(cudaGraphLaunch(graph, cs), "graph launch");
         } else {
+            pdl_off g(eager_no_pdl);
             enqueue_round();
         }
         if (last && host_out)
