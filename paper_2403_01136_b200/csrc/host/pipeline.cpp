@@ -666,6 +666,32 @@ struct pipeline::impl {
         if (evs) cuda_ok(timing_record(evs[i], cs), "ev");
     }
 
+    // HP_PIPE_TRACE=1 (eager rounds only): an event after every launch, so
+    // the watchdog can name the first kernel that did not complete
+    bool trace_on = [] {
+        const char* e = std::getenv("HP_PIPE_TRACE");
+        return e && *e && *e != '0';
+    }();
+    std::vector<cudaEvent_t> trace_ev;
+    std::vector<std::string> trace_what;
+    size_t trace_n = 0;
+    int trace_unit = -1;
+    void tr(const char* what, int li = -1) {
+        if (!trace_on) return;
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        cuda_ok(cudaStreamIsCapturing(cs, &cap), "capture status");
+        if (cap != cudaStreamCaptureStatusNone) return;
+        if (trace_n == trace_ev.size()) {
+            cudaEvent_t e;
+            cuda_ok(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "trace ev");
+            trace_ev.push_back(e);
+            trace_what.emplace_back();
+        }
+        trace_what[trace_n] = "unit " + std::to_string(trace_unit) + " layer " + std::to_string(li) + " " + what;
+        cuda_ok(cudaEventRecord(trace_ev[trace_n], cs), "trace ev");
+        ++trace_n;
+    }
+
     void qlin(const opw& w, const void* x, int64_t ldx, int64_t m, void* y, int64_t ldy,
               const void* res, int epi, int phase) {
         hp_ok(hp_qlinear(&w.w, x, ldx, m, y, ldy, res, res ? ldy : 0, epi, phase, ws, ws_bytes, cs),
@@ -687,8 +713,10 @@ struct pipeline::impl {
             cuda_ok(hp::launch_layernorm(x, h1, m, static_cast<int>(h1), L.ln[0], L.ln[1], scr_a,
                                          h1, cs),
                     "ln1");
+            tr("ln1", static_cast<int>(li));
             record(ev, 0);
             qlin(L.ops[0], scr_a, h1, m, scr_qkv, 3 * h1, nullptr, HP_EPI_NONE, phase);
+            tr("qkv", static_cast<int>(li));
             record(ev, 1);
             // causal multi-head attention over the KV cache -> scr_a
             if (phase == HP_PREFILL) {
@@ -701,18 +729,23 @@ struct pipeline::impl {
                                                attn_split),
                         "attention (decode)");
             }
+            tr("attention", static_cast<int>(li));
             record(ev, 8);
             record(ev, 2);
             qlin(L.ops[1], scr_a, h1, m, x, h1, x, HP_EPI_NONE, phase);
+            tr("out", static_cast<int>(li));
             record(ev, 3);
             cuda_ok(hp::launch_layernorm(x, h1, m, static_cast<int>(h1), L.ln[2], L.ln[3], scr_a,
                                          h1, cs),
                     "ln2");
+            tr("ln2", static_cast<int>(li));
             record(ev, 4);
             qlin(L.ops[2], scr_a, h1, m, scr_f, h2, nullptr, HP_EPI_RELU, phase);
+            tr("fc1", static_cast<int>(li));
             record(ev, 5);
             record(ev, 6);
             qlin(L.ops[3], scr_f, h2, m, x, h1, x, HP_EPI_NONE, phase);
+            tr("fc2", static_cast<int>(li));
             record(ev, 7);
             if (instrument) cuda_ok(timing_record(lay_ev[phase][2 * li + 1], cs), "ev");
         }
@@ -876,6 +909,7 @@ struct pipeline::impl {
                 recv_idx[{static_cast<int>(u.kind), u.index, u.token}] = static_cast<int>(i);
             }
         }
+        trace_n = 0;
         microbatch_manager mbm(B, eta, xi, n);  // the round's status table
         int comp_i = 0;
 
@@ -896,14 +930,17 @@ struct pipeline::impl {
             const unit_ctx ctx = pre ? unit_ctx{u.index * eta, sched.prefill_sizes[u.index], -1}
                                      : unit_ctx{group_first[u.index], group_size[u.index], s + u.token - 1};
             cuda_ok(timing_record(unit_ev[2 * ui], cs), "ev");
+            trace_unit = static_cast<int>(ui);
             if (first) {
                 if (pre) embed_prefill(u.index);
                 else embed_decode(u.index, u.token);
+                tr("embed");
             }
             forward(x, m, phase, opt.instrument && instr_unit[phase] == static_cast<int>(ui), ctx);
             if (last) {
                 if (pre) lm_head(x, s, s - 1, sched.prefill_sizes[u.index], ctx.req0, 0);
                 else lm_head(x, 1, 0, group_size[u.index], ctx.req0, u.token);
+                tr("lm_head+argmax");
             }
             cuda_ok(timing_record(unit_ev[2 * ui + 1], cs), "ev");
 
@@ -968,6 +1005,13 @@ struct pipeline::impl {
             const unit_ref& u = units[u_done];
             msg += ", stuck at unit (" + std::string(u.kind == pipesim::unit_kind::prefill ? "prefill" : "decode") +
                    " " + std::to_string(u.index) + " token " + std::to_string(u.token) + ")";
+        }
+        if (trace_n) {
+            size_t t = 0;
+            while (t < trace_n && done(trace_ev[t])) ++t;
+            msg += t < trace_n ? ", first pending launch: " + trace_what[t] +
+                                     (t ? " (last completed: " + trace_what[t - 1] + ")" : std::string())
+                               : std::string(", every traced launch completed");
         }
         timed_out = true;
         throw pipeline_timeout(msg);
@@ -1129,7 +1173,7 @@ struct pipeline::impl {
                         static_cast<void*>(cur_tok), prompt, scr_a, scr_qkv, scr_f, ws, attn_ws})
             f(p);
         for (void* p : dec_x) f(p);
-        for (auto* v : {&unit_ev, &recv_ev, &comp_ev, &op_ev[0], &op_ev[1], &lay_ev[0], &lay_ev[1]})
+        for (auto* v : {&unit_ev, &recv_ev, &comp_ev, &op_ev[0], &op_ev[1], &lay_ev[0], &lay_ev[1], &trace_ev})
             for (cudaEvent_t e : *v) cudaEventDestroy(e);
         for (cudaEvent_t e : {ev_t0, ev_t1, ev_fork, ev_join_s, ev_join_r})
             if (e) cudaEventDestroy(e);
