@@ -771,12 +771,16 @@ struct pipeline::impl {
     void lm_head(const void* x, int64_t stride, int64_t off, int rows, int req0, int col) {
         cuda_ok(hp::launch_gather_rows(x, h1, stride, off, rows, static_cast<int>(h1), lm_x, h1, cs),
                 "gather");
+        tr("gather");
         cuda_ok(hp::launch_layernorm(lm_x, h1, rows, static_cast<int>(h1), lnf[0], lnf[1], lm_a, h1, cs),
                 "final ln");
+        tr("final ln");
         qlin(lm, lm_a, h1, rows, logits, vocab, nullptr, HP_EPI_NONE, HP_DECODE);
+        tr("lm head");
         cuda_ok(hp::launch_argmax(logits, vocab, rows, vocab, cur_tok + req0,
                                   out_tok + static_cast<size_t>(req0) * n + col, n, cs),
                 "argmax");
+        tr("argmax");
     }
 
     // every distinct (rows, phase) the round's units run with
@@ -940,7 +944,6 @@ struct pipeline::impl {
             if (last) {
                 if (pre) lm_head(x, s, s - 1, sched.prefill_sizes[u.index], ctx.req0, 0);
                 else lm_head(x, 1, 0, group_size[u.index], ctx.req0, u.token);
-                tr("lm_head+argmax");
             }
             cuda_ok(timing_record(unit_ev[2 * ui + 1], cs), "ev");
 
